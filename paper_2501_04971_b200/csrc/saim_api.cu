@@ -1,0 +1,368 @@
+// saim_api.cu -- host side of libsaim (C ABI declared in include/saim.h).
+//
+// saim_create: validation, slack extension, normalisation scales,
+// integer-range proofs (DESIGN.md Appendix B), and the HBM layout of saim_layout.h.
+// saim_run: argument checks and the asynchronous launches (init + fused SAIM kernel) on the
+// caller's stream.  No arithmetic of the sweep happens on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/saim.h"
+#include "saim_layout.h"
+
+namespace saim {
+int qkp_npl_bucket(int npl);
+cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *max_wpc);
+cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st);
+int mkp_plan(int n, int M, int n_slack_max, int *lanes, int *smem_bytes, int *max_wpc);
+cudaError_t mkp_launch(const RunArgs &a, int n_inst, int lanes, int wpc, int smem_bytes, cudaStream_t st);
+void mkp_blob_layout(int n, int M, int n_slack_max, uint32_t *a_off, uint32_t *c_off, uint32_t *x_off, uint32_t *bytes);
+int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
+}  // namespace saim
+
+using namespace saim;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char *what) {
+  return fail(SAIM_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct saim_ctx {
+  int device = 0;
+  int n_inst = 0, n = 0, M = 0;
+  int kernel = 0;       // 1 = QKP, 2 = MKP
+  int npl = 0, qb = 0;  // QKP
+  int lanes = 32;       // MKP lanes per replica
+  int N_max = 0, n_slack_max = 0;
+  int smem_bytes = 0, max_wpc = 32, sm_count = 148;
+  uint32_t blob_bytes = 0, a_off = 0, c_off = 0, x_off = 0;
+  double beta_max = 0, eta = 0;
+  long long r_abs_max = 0;
+  unsigned char *d_blob = nullptr;
+  InstHdr *d_hdr = nullptr;
+  std::vector<InstHdr> hdr;
+  std::vector<std::vector<int32_t>> q;  // slack bits per row per instance
+};
+
+static int bit_length(long long v) {
+  int q = 0;
+  while (v > 0) { ++q; v >>= 1; }
+  return q;
+}
+
+static uint32_t align16(uint32_t v) { return (v + 15u) & ~15u; }
+
+__global__ void saim_init_outputs(int64_t *inst_best, int n_inst, uint64_t *counters) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (inst_best && i < n_inst) inst_best[i] = LLONG_MAX;
+  if (counters && i < SAIM_NUM_COUNTERS) counters[i] = 0;
+}
+
+extern "C" const char *saim_last_error(void) { return g_err.c_str(); }
+
+extern "C" int saim_create(const saim_problem *prob, const saim_params *par, saim_ctx **out) {
+  g_err.clear();
+  if (!prob || !par || !out) return fail(SAIM_EINVAL, "null argument");
+  *out = nullptr;
+  const int S = prob->n_inst, n = prob->n_items, M = prob->n_cons;
+  if (S < 1 || S >= 4096) return fail(SAIM_EINVAL, "n_inst must be in [1, 4096) (RNG counter field), got %d", S);
+  if (n < 1) return fail(SAIM_EINVAL, "n_items must be >= 1");
+  if (M < 0 || M > 32) return fail(SAIM_EINVAL, "n_cons must be in [0, 32], got %d", M);
+  if (!prob->c || (M > 0 && (!prob->A || !prob->b)) || !par->P)
+    return fail(SAIM_EINVAL, "missing c/A/b/P array");
+  if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
+  if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
+
+  if (M > 1 && prob->Q)
+    return fail(SAIM_EUNSUPPORTED, "quadratic objective with M = %d > 1 constraints has no kernel", M);
+
+  saim_ctx *ctx = new saim_ctx();
+  ctx->device = par->device;
+  ctx->n_inst = S; ctx->n = n; ctx->M = M;
+  ctx->beta_max = par->beta_max; ctx->eta = par->eta;
+  ctx->hdr.resize(S);
+  ctx->q.resize(S);
+
+  // ---- per-instance validation, slack, scales, range proofs ----
+  long long rmax_all = 0;
+  int qmax_abs = 0;
+  for (int s = 0; s < S; ++s) {
+    const int32_t *Q = prob->Q ? prob->Q + (size_t)s * n * n : nullptr;
+    const int32_t *c = prob->c + (size_t)s * n;
+    const int32_t *A = M ? prob->A + (size_t)s * M * n : nullptr;
+    const int64_t *b = M ? prob->b + (size_t)s * M : nullptr;
+    const double P = par->P[s];
+    if (!std::isfinite(P) || P < 0) { delete ctx; return fail(SAIM_EINVAL, "P[%d] must be finite and >= 0", s); }
+    long long so = 0, sc = 0;
+    long long phi_bound = 0;
+    for (int i = 0; i < n; ++i) {
+      long long rowsum = std::llabs((long long)c[i]);
+      so = std::max(so, std::llabs((long long)c[i]));
+      if (Q) {
+        if (Q[(size_t)i * n + i] != 0) { delete ctx; return fail(SAIM_EINVAL, "Q[%d] has a nonzero diagonal at %d", s, i); }
+        for (int j = 0; j < n; ++j) {
+          const long long qij = Q[(size_t)i * n + j];
+          if (qij != Q[(size_t)j * n + i]) { delete ctx; return fail(SAIM_EINVAL, "Q[%d] is not symmetric at (%d,%d)", s, i, j); }
+          so = std::max(so, std::llabs(qij));
+          rowsum += std::llabs(qij);
+          qmax_abs = (int)std::max<long long>(qmax_abs, std::llabs(qij));
+        }
+      }
+      phi_bound = std::max(phi_bound, rowsum);
+    }
+    int n_slack = 0;
+    long long rmax = 0;
+    for (int k = 0; k < M; ++k) {
+      if (b[k] < 1) { delete ctx; return fail(SAIM_EINVAL, "b[%d][%d] must be >= 1", s, k); }
+      sc = std::max(sc, (long long)b[k]);
+      long long load = 0;
+      for (int j = 0; j < n; ++j) {
+        const long long v = A[(size_t)k * n + j];
+        if (v < 0) { delete ctx; return fail(SAIM_EINVAL, "A[%d] has a negative entry", s); }
+        sc = std::max(sc, v);
+        load += v;
+      }
+      const int q = bit_length(b[k]);  // Q = floor(log2 b + 1)
+      ctx->q[s].push_back(q);
+      n_slack += q;
+      const long long slack_max = (1LL << q) - 1;
+      rmax = std::max(rmax, std::max((long long)b[k], load + slack_max - b[k]));
+    }
+    if (so == 0) so = 1;
+    if (sc == 0) sc = 1;
+    rmax_all = std::max(rmax_all, rmax);
+    InstHdr &h = ctx->hdr[s];
+    memset(&h, 0, sizeof(h));
+    h.N = n + n_slack;
+    h.n_slack = n_slack;
+    h.b0 = M ? b[0] : 0;
+    h.s_o = so; h.s_c = sc;
+    h.c_o = 1.0 / (double)so;
+    h.c_p = P / ((double)sc * (double)sc);
+    h.c_l = par->eta / ((double)sc * (double)sc);
+    ctx->N_max = std::max(ctx->N_max, h.N);
+    ctx->n_slack_max = std::max(ctx->n_slack_max, n_slack);
+    // exactness proofs (DESIGN.md Appendix B)
+    if (phi_bound >= (1LL << 22))
+      { delete ctx; return fail(SAIM_ERANGE, "instance %d: |phi| bound %lld >= 2^22", s, phi_bound); }
+    if (rmax >= (1LL << 21))
+      { delete ctx; return fail(SAIM_ERANGE, "instance %d: |r| bound %lld >= 2^21", s, rmax); }
+    long long fb = 0;
+    for (int i = 0; i < n; ++i) fb += std::llabs((long long)c[i]) + (Q ? phi_bound : 0);
+    if (fb >= (1LL << 42)) { delete ctx; return fail(SAIM_ERANGE, "instance %d: |f| bound >= 2^42", s); }
+  }
+  ctx->r_abs_max = rmax_all;
+  if (ctx->N_max > 2048) { delete ctx; return fail(SAIM_ESMEM, "N = %d spins > 2048", ctx->N_max); }
+
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaSetDevice"); }
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device);
+
+  std::vector<unsigned char> blob;
+  if (M <= 1) {
+    // ---------------- QKP kernel layout ----------------
+    ctx->kernel = 1;
+    const int npl = (n + 31) / 32;
+    ctx->npl = qkp_npl_bucket(npl);
+    if (ctx->npl < 0) { delete ctx; return fail(SAIM_ESMEM, "n = %d items > 512 (Q does not fit shared memory)", n); }
+    ctx->qb = qmax_abs <= 127 ? 1 : (qmax_abs <= 32767 ? 2 : 0);
+    if (!ctx->qb) { delete ctx; return fail(SAIM_ERANGE, "|Q| entries > 32767 need wider storage"); }
+    const int E = 4 / ctx->qb;
+    const int QW = (ctx->npl + E - 1) / E;
+    const int NBM = ctx->npl + 2;
+    const uint32_t q_bytes = align16((uint32_t)n * QW * 128u);
+    ctx->a_off = q_bytes;
+    ctx->c_off = ctx->a_off + align16(NBM * 32 * 4);
+    ctx->blob_bytes = ctx->c_off + align16(ctx->npl * 32 * 4);
+    if ((int)ctx->blob_bytes + 64 > smem_optin) {
+      delete ctx;
+      return fail(SAIM_ESMEM, "QKP blob of %u bytes exceeds shared memory (%d)", ctx->blob_bytes, smem_optin);
+    }
+    ctx->smem_bytes = (int)ctx->blob_bytes;
+    blob.assign((size_t)S * ctx->blob_bytes, 0);
+    const uint32_t bias = 1u << (8 * ctx->qb - 1);
+    for (int s = 0; s < S; ++s) {
+      unsigned char *B = blob.data() + (size_t)s * ctx->blob_bytes;
+      const int32_t *Q = prob->Q ? prob->Q + (size_t)s * n * n : nullptr;
+      for (int j = 0; j < n; ++j) {
+        uint32_t *row = reinterpret_cast<uint32_t *>(B + (size_t)j * QW * 128u);
+        for (int w = 0; w < QW; ++w)
+          for (int l = 0; l < 32; ++l) {
+            uint32_t word = 0;
+            for (int e2 = 0; e2 < E; ++e2) {
+              const int m = E * w + e2, i = 32 * m + l;
+              const long long qv = (Q && i < n) ? Q[(size_t)j * n + i] : 0;
+              word |= ((uint32_t)(qv + bias) & ((1u << (8 * ctx->qb)) - 1u)) << (8 * ctx->qb * e2);
+            }
+            row[32 * w + l] = word;
+          }
+      }
+      float *Aext = reinterpret_cast<float *>(B + ctx->a_off);
+      if (M == 1) {
+        const int32_t *A = prob->A + (size_t)s * n;
+        for (int i = 0; i < n; ++i) Aext[i] = (float)A[i];
+        const int q = ctx->q[s][0];
+        for (int bit = 0; bit < q; ++bit) Aext[n + bit] = (float)(1LL << bit);
+      }
+      int32_t *cc = reinterpret_cast<int32_t *>(B + ctx->c_off);
+      for (int i = 0; i < n; ++i) cc[i] = prob->c[(size_t)s * n + i];
+    }
+    e = qkp_configure(ctx->npl, ctx->qb, ctx->smem_bytes, smem_optin, &ctx->max_wpc);
+    if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "configure QKP kernel"); }
+    ctx->lanes = 32;
+  } else if (!prob->Q) {
+    // ---------------- MKP kernel layout ----------------
+    ctx->kernel = 2;
+    int lanes = 0, smem = 0, mw = 0;
+    if (mkp_plan(n, M, ctx->n_slack_max, &lanes, &smem, &mw) != 0 || smem + 64 > smem_optin) {
+      delete ctx;
+      return fail(SAIM_ESMEM, "MKP instance (n=%d, M=%d) does not fit shared memory", n, M);
+    }
+    for (int s = 0; s < S; ++s)
+      for (int k = 0; k < M; ++k)
+        for (int j = 0; j < n; ++j)
+          if (prob->A[((size_t)s * M + k) * n + j] > 32767) {
+            delete ctx;
+            return fail(SAIM_ERANGE, "MKP weights must be <= 32767 (int16 columns)");
+          }
+    ctx->lanes = lanes; ctx->smem_bytes = smem; ctx->max_wpc = mw;
+    mkp_blob_layout(n, M, ctx->n_slack_max, &ctx->a_off, &ctx->c_off, &ctx->x_off, &ctx->blob_bytes);
+    blob.assign((size_t)S * ctx->blob_bytes, 0);
+    const int n_pad = (n + 1) & ~1;
+    for (int s = 0; s < S; ++s) {
+      unsigned char *B = blob.data() + (size_t)s * ctx->blob_bytes;
+      int16_t *Acol = reinterpret_cast<int16_t *>(B + ctx->a_off);      // [n_pad][M]
+      for (int j = 0; j < n; ++j)
+        for (int k = 0; k < M; ++k) Acol[(size_t)j * M + k] = (int16_t)prob->A[((size_t)s * M + k) * n + j];
+      int32_t *cc = reinterpret_cast<int32_t *>(B + ctx->c_off);
+      for (int i = 0; i < n; ++i) cc[i] = prob->c[(size_t)s * n + i];
+      (void)n_pad;
+      uint16_t *sl = reinterpret_cast<uint16_t *>(B + ctx->x_off);       // (row << 8) | shift
+      int idx = 0;
+      for (int k = 0; k < M; ++k)
+        for (int bit = 0; bit < ctx->q[s][k]; ++bit) sl[idx++] = (uint16_t)((k << 8) | bit);
+    }
+  } else {
+    delete ctx;
+    return fail(SAIM_EUNSUPPORTED, "quadratic objective with M = %d > 1 constraints has no kernel", M);
+  }
+
+  e = cudaMalloc(&ctx->d_blob, blob.size());
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaMalloc blob"); }
+  e = cudaMalloc(&ctx->d_hdr, sizeof(InstHdr) * S);
+  if (e != cudaSuccess) { cudaFree(ctx->d_blob); delete ctx; return cuda_fail(e, "cudaMalloc hdr"); }
+  e = cudaMemcpy(ctx->d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_hdr, ctx->hdr.data(), sizeof(InstHdr) * S, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { saim_destroy(ctx); return cuda_fail(e, "upload"); }
+  *out = ctx;
+  return SAIM_OK;
+}
+
+extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, int32_t K, int32_t T,
+                        void *cuda_stream, const saim_outputs *out) {
+  g_err.clear();
+  if (!ctx || !out) return fail(SAIM_EINVAL, "null argument");
+  if (R < 1 || rep0 < 0 || (long long)rep0 + R > (1LL << 20))
+    return fail(SAIM_EINVAL, "replicas must satisfy 1 <= R and rep0 + R <= 2^20");
+  if (K < 1 || T < 1) return fail(SAIM_EINVAL, "K and T must be >= 1");
+  if (!out->best_f || !out->best_x || !out->best_k || !out->n_feasible)
+    return fail(SAIM_EINVAL, "best_f, best_x, best_k and n_feasible are required");
+  if ((double)K * (double)(ctx->r_abs_max + 1) >= 4.0e18)
+    return fail(SAIM_ERANGE, "K * max|r| would overflow the int64 Lagrange accumulator");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  e = cudaGetLastError();  // surface earlier asynchronous faults
+  if (e != cudaSuccess) return cuda_fail(e, "pending CUDA error");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+
+  RunArgs a;
+  memset(&a, 0, sizeof(a));
+  a.blob = ctx->d_blob; a.hdr = ctx->d_hdr; a.blob_bytes = ctx->blob_bytes;
+  a.a_off = ctx->a_off; a.c_off = ctx->c_off; a.x_off = ctx->x_off;
+  a.n = ctx->n; a.M = ctx->M;
+  a.Wn = (ctx->n + 31) / 32; a.WN = (ctx->N_max + 31) / 32;
+  a.R = R; a.rep0 = rep0; a.K = K; a.T = T;
+  a.seed = seed; a.beta_max = ctx->beta_max;
+  a.out = *out;
+
+  saim_init_outputs<<<(ctx->n_inst + 255) / 256, 256, 0, st>>>(out->inst_best, ctx->n_inst, out->counters);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "init launch");
+
+  if (ctx->kernel == 1) {
+    const long long warps = (long long)R * ctx->n_inst;
+    int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
+    wpc = std::max(1, std::min(wpc, ctx->max_wpc));
+    e = qkp_launch(ctx->npl, ctx->qb, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
+  } else {
+    const int rpw = 32 / ctx->lanes;                     // replicas per warp
+    const long long warps = ((long long)R * ctx->n_inst + rpw - 1) / rpw;
+    int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
+    wpc = std::max(1, std::min(wpc, ctx->max_wpc));
+    e = mkp_launch(a, ctx->n_inst, ctx->lanes, wpc, ctx->smem_bytes, st);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  return SAIM_OK;
+}
+
+extern "C" int saim_get_info(const saim_ctx *ctx, saim_info *out) {
+  if (!ctx || !out) return fail(SAIM_EINVAL, "null argument");
+  out->n_inst = ctx->n_inst; out->n_items = ctx->n; out->n_cons = ctx->M;
+  out->n_spins_max = ctx->N_max;
+  out->words_items = (ctx->n + 31) / 32;
+  out->words_full = (ctx->N_max + 31) / 32;
+  out->kernel = ctx->kernel;
+  out->smem_bytes = ctx->smem_bytes;
+  out->q_bytes = ctx->kernel == 1 ? ctx->qb : 0;
+  out->lanes_per_replica = ctx->lanes;
+  return SAIM_OK;
+}
+
+extern "C" int saim_get_instance(const saim_ctx *ctx, int32_t inst, int32_t *N, int64_t *s_o, int64_t *s_c, int32_t *q) {
+  if (!ctx || inst < 0 || inst >= ctx->n_inst) return fail(SAIM_EINVAL, "bad instance index");
+  const InstHdr &h = ctx->hdr[inst];
+  if (N) *N = h.N;
+  if (s_o) *s_o = h.s_o;
+  if (s_c) *s_c = h.s_c;
+  if (q) for (int k = 0; k < ctx->M; ++k) q[k] = ctx->q[inst][k];
+  return SAIM_OK;
+}
+
+extern "C" void saim_destroy(saim_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->d_blob) cudaFree(ctx->d_blob);
+  if (ctx->d_hdr) cudaFree(ctx->d_hdr);
+  delete ctx;
+}
+
+extern "C" int saim_selftest(int which, int device, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64) {
+  g_err.clear();
+  if ((which == 0 && (n < 1 || !in_u32 || !out_u32)) || (which == 1 && !out_f64) || which < 0 || which > 1)
+    return fail(SAIM_EINVAL, "bad selftest arguments");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  if (selftest(which, n, in_u32, out_u32, out_f64) != 0) return fail(SAIM_ECUDA, "selftest failed");
+  return SAIM_OK;
+}

@@ -1,0 +1,379 @@
+// saim_qkp.cu -- fused SAIM kernel for problems with a quadratic objective and M <= 1
+// constraint (QKP; BASELINE.json configs 0-2).  sm_100a.
+//
+// One warp = one replica (an independent SAIM chain, R22); one CTA = up to 32 replicas of the
+// same instance sharing that instance's Q, A_ext and c in shared memory (TMA bulk-staged once).
+// The whole of Algorithm 1 runs inside the kernel: K anneals of T sweeps of
+// N sequential p-bit decisions (Eq. 9-10), per-anneal readout, best
+// tracking and the Lagrange step.  Nothing crosses the host boundary between iterations.
+//
+// Exact sequential semantics with 32 lanes: lane l owns the
+// spins i = 32b + l.  For block b every pending lane evaluates its decision against the current
+// state; a ballot finds the first lane whose decision flips its spin; decisions of the lanes
+// before it (and its own) are final -- they were taken on exactly the state the sequential sweep
+// would have seen.  The flip is applied (phi_j -= delta Q_ij for every item j, r += delta A_i) and
+// the lanes after it re-evaluate with the SAME uniforms (counter-based Philox, R2).  A block
+// costs 1 + (#flips in it) rounds.
+//
+// Field of spin i in binary form (R1): F_i = c_o phi_i - A_i (c_p v_i + c_l Lambda), with
+// v_i = 2 r0 + A_i = 2r + A_i (1 - 2 x_i) (Eq. 3 and Eq. 5 differences, M = 1), z = beta_t F_i.
+// phi_i, r, v_i are exact integers held in fp32 (|.| < 2^22, proved on the host).  The decision
+// [u < sigma(z)] <=> [z > logit(u)] is taken in fp32 with a rigorous error bound e: saturated
+// when |z| - e > ln(2^24-1) (no uniform needed, R19), else compared with logit(u) evaluated with
+// MUFU lg2; inside the combined error band it is re-done in fp64 (R18).
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "saim_dev.cuh"
+
+namespace saim {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+// |logit_f32(u) - logit(u)| <= kLogitAbs + kLogitRel * |logit(u)| for every representable u
+// (checked exhaustively over all 2^23 uniforms by tests/test_gpu_kernels.py).
+constexpr float kLogitAbs = 0x1p-17f;
+constexpr float kLogitRel = 0x1p-19f;
+// fp32 field: |z_f32 - z| <= kZRel * S with S = |K1 phi| + |A|(|K2 v| + |K3|); the true bound
+// is ~3 * 2^-24 (three roundings + fp32 constants), kZRel leaves a 5x margin.
+constexpr float kZRel = 0x1p-20f;
+
+__device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
+  return i == 0 ? u.x : (i == 1 ? u.y : (i == 2 ? u.z : u.w));
+}
+
+__device__ __forceinline__ float logit_f32(uint32_t w) {
+  const float u = uniform_f32(w);
+  return (__log2f(u) - __log2f(1.0f - u)) * 0.693147180559945309f;
+}
+
+struct Cnt {
+  uint32_t rounds = 0, flips = 0, unif = 0, fp64 = 0, uncert = 0, philox = 0;
+};
+
+// fp64 re-evaluation of one decision (R18 slow path).  beta is recomputed exactly as
+// the fast path's constants were derived (beta_max * t / (T-1)).
+__device__ __noinline__ int decide_fp64(float phib, float v, float A, double beta, double c_o, double c_p,
+                                        double LC, uint32_t w, uint32_t *uncert) {
+  const double K1d = beta * c_o, K2d = beta * c_p, K3d = beta * LC;
+  const double Ad = (double)A, vd = (double)v, pd = (double)phib;
+  const double z = fma(K1d, pd, -(Ad * fma(K2d, vd, K3d)));
+  const double S = fabs(K1d * pd) + fabs(Ad) * (fabs(K2d * vd) + fabs(K3d));
+  const double u = uniform_f64(w);
+  const double l = log(u) - log1p(-u);
+  const double d = z - l;
+  const double e = (S + 1.0 + fabs(l)) * 0x1p-47;
+  if (fabs(d) <= e) ++*uncert;
+  return d > 0.0;
+}
+
+}  // namespace
+
+// Shared memory: [instance blob: Q rows | A_ext | c] [phi: warps x NPL*32 floats]
+template <int NPL, int QB>
+__global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
+  constexpr int E = 4 / QB;                          // Q entries per 32-bit word
+  constexpr int QW = (NPL + E - 1) / E;              // words per lane per Q row
+  constexpr uint32_t kRowBytes = QW * 128u;
+  constexpr float kQBias = (float)(1 << (8 * QB - 1));
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t mbar;
+
+  const int s = blockIdx.y;
+  bulk_stage(smem, a.blob + (size_t)s * a.blob_bytes, a.blob_bytes, &mbar);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ridx = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (ridx >= a.R) return;
+  const int rho = a.rep0 + ridx;
+  const InstHdr H = a.hdr[s];
+  const unsigned char *sQ = smem;
+  const float *sA = reinterpret_cast<const float *>(smem + a.a_off);
+  const int32_t *sC = reinterpret_cast<const int32_t *>(smem + a.c_off);
+  float *phw = reinterpret_cast<float *>(smem + a.blob_bytes) + warp * (NPL * 32) + lane;  // phi[32m + lane]
+  const int n = a.n, N = H.N, NB = (N + 31) >> 5;
+  const bool has_con = a.M > 0;
+
+#pragma unroll
+  for (int m = 0; m < NPL; ++m) phw[32 * m] = (32 * m + lane < n) ? (float)(-sC[32 * m + lane]) : 0.0f;  // x = 0
+  uint64_t xm = 0;                                  // bit b = x_{32b + lane}
+  float r = has_con ? (float)(-H.b0) : 0.0f;        // r = A_ext x - b (exact integer)
+  long long Lam = 0;                                // Lambda_0 = 0 (lambda_0 = 0)
+  long long best_f = LLONG_MAX;
+  int best_k = -1, nfeas = 0;
+  uint32_t best_word = 0;
+  Cnt cn;
+
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
+
+  // Flip of spin j = 32b + L by delta = dl (+1/-1): Eq. 9 in incremental form.
+  auto apply_flip = [&](int b, int L, float AL, float dl) {
+    r = fmaf(dl, AL, r);
+    if (lane == L) xm ^= (1ull << b);
+    const int j = 32 * b + L;
+    if (j < n) {
+      const uint32_t *row = reinterpret_cast<const uint32_t *>(sQ + (size_t)j * kRowBytes) + lane;
+#pragma unroll
+      for (int w = 0; w < QW; ++w) {
+        const uint32_t word = row[32 * w];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int m = E * w + e;
+          if (m < NPL) {
+            const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
+            const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
+            phw[32 * m] = fmaf(-dl, q, phw[32 * m]);
+          }
+        }
+      }
+    }
+    ++cn.flips;
+  };
+
+  for (int k = 0; k < a.K; ++k) {
+    const double LC = H.c_l * (double)Lam;           // c_l Lambda = (eta/s_c^2) Lambda
+    for (int t = 0; t < a.T; ++t) {
+      const double beta = (a.T >= 2) ? a.beta_max * (double)t / (double)(a.T - 1) : a.beta_max;
+      const bool bz = (a.T >= 2) && (t == 0);        // beta_0 = 0: x_i = [u < 1/2]
+      const float K1 = (float)(beta * H.c_o), K2 = (float)(beta * H.c_p), K3 = (float)(beta * LC);
+      uint4 uw = make_uint4(0, 0, 0, 0);
+      bool have_u = false;
+      for (int b = 0; b < NB; ++b) {
+        if ((b & 3) == 0) have_u = false;
+        const int nvalid = N - 32 * b;
+        uint32_t pending = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
+        const bool valid = lane < nvalid;
+        const float A = valid ? sA[32 * b + lane] : 0.0f;
+        int xb = (int)((xm >> b) & 1ull);
+        if (bz) {
+          if (!have_u) { uw = philox_group(key, b >> 2, lane, t, k, srho); have_u = true; cn.philox += 32; }
+          const int nx = (sel4(uw, b & 3) >> 31) == 0u;   // u < 1/2  <=>  w < 2^31
+          uint32_t fm = __ballot_sync(kFull, valid && nx != xb);
+          cn.unif += __popc(pending);
+          ++cn.rounds;
+          while (fm) {                                      // decisions are state-independent
+            const int L = __ffs(fm) - 1;
+            fm &= fm - 1u;
+            apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+          }
+          continue;
+        }
+        const float AK2 = A * K2, AK3 = A * K3;
+        const float aAK2 = fabsf(AK2), aAK3 = fabsf(AK3);
+        const bool item_blk = 32 * b < n;
+        for (;;) {
+          ++cn.rounds;
+          const float phib = item_blk ? phw[32 * b] : 0.0f;
+          const float v = fmaf(A, xb ? -1.0f : 1.0f, 2.0f * r);
+          const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));
+          const float S = fmaf(K1, fabsf(phib), fmaf(aAK2, fabsf(v), aAK3));
+          const float e = S * kZRel;
+          const bool mine = (pending >> lane) & 1u;
+          const bool sat = fabsf(z) - e > kSatThr;
+          int nx = z > 0.0f;
+          const uint32_t need = __ballot_sync(kFull, mine && !sat);
+          if (need) {
+            if (!have_u) { uw = philox_group(key, b >> 2, lane, t, k, srho); have_u = true; cn.philox += 32; }
+            cn.unif += __popc(need);
+            if (mine && !sat) {
+              const uint32_t w = sel4(uw, b & 3);
+              const float l = logit_f32(w);
+              const float d = z - l;
+              const float el = kLogitAbs + kLogitRel * fabsf(l);
+              if (fabsf(d) > (e + el) * 1.0001f) {
+                nx = d > 0.0f;
+              } else {
+                ++cn.fp64;
+                nx = decide_fp64(phib, v, A, beta, H.c_o, H.c_p, LC, w, &cn.uncert);
+              }
+            }
+          }
+          const uint32_t fm = __ballot_sync(kFull, mine && nx != xb);
+          if (!fm) break;
+          const int L = __ffs(fm) - 1;
+          apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+          if (lane == L) xb ^= 1;
+          pending &= ~((2u << L) - 1u);
+          if (!pending) break;
+        }
+      }
+    }
+    // ---- readout of x_k (Algorithm 1 "store feasible") ----
+    int fpart = 0, load = 0;
+#pragma unroll
+    for (int m = 0; m < NPL; ++m) {
+      if (((xm >> m) & 1ull) && 32 * m + lane < n) {
+        fpart += sC[32 * m + lane] - (int)phw[32 * m];      // x_i (c_i - phi_i)
+        load += (int)sA[32 * m + lane];
+      }
+    }
+    const long long f = warp_sum_i64((long long)fpart) / 2;  // f = 1/2 sum_i x_i (c_i - phi_i)
+    load = __reduce_add_sync(kFull, load);
+    const bool feas = !has_con || (long long)load <= H.b0;
+    uint32_t myword = 0;
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1ull);
+      if (lane == b) myword = wb;
+    }
+    const long long rl = (long long)r;
+    const size_t row = ((size_t)s * a.R + ridx) * a.K + k;
+    if (lane == 0) {
+      if (a.out.tr_f) a.out.tr_f[row] = f;
+      if (a.out.tr_feas) a.out.tr_feas[row] = (uint8_t)feas;
+      if (has_con && a.out.tr_r) a.out.tr_r[row] = rl;
+      if (has_con && a.out.tr_lam) a.out.tr_lam[row] = Lam;
+    }
+    if (a.out.tr_x && lane < a.WN) a.out.tr_x[row * a.WN + lane] = myword;
+    if (feas) {
+      ++nfeas;
+      if (f < best_f) {
+        best_f = f;
+        best_k = k;
+        const int rem = n - 32 * lane;
+        best_word = rem >= 32 ? myword : (rem > 0 ? (myword & ((1u << rem) - 1u)) : 0u);
+      }
+    }
+    Lam += rl;                                               // lambda_{k+1} = lambda_k + eta g(x_k)
+  }
+
+  // ---- outputs ----
+  const size_t ri = (size_t)s * a.R + ridx;
+  if (lane == 0) {
+    a.out.best_f[ri] = best_f;
+    a.out.best_k[ri] = best_k;
+    a.out.n_feasible[ri] = nfeas;
+    if (best_k >= 0 && a.out.inst_best)
+      atomicMin(reinterpret_cast<long long *>(a.out.inst_best) + s, (best_f << 20) | (long long)rho);
+    if (has_con && a.out.final_lam) a.out.final_lam[ri] = Lam;
+  }
+  if (lane < a.Wn) a.out.best_x[ri * a.Wn + lane] = best_word;
+  if (a.out.final_x) {
+    uint32_t myword = 0;
+    for (int b = 0; b < NB; ++b) {
+      const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1ull);
+      if (lane == b) myword = wb;
+    }
+    if (lane < a.WN) a.out.final_x[ri * a.WN + lane] = myword;
+  }
+  const uint32_t fp64 = __reduce_add_sync(kFull, cn.fp64), unc = __reduce_add_sync(kFull, cn.uncert);
+  if (lane == 0 && a.out.counters) {
+    unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
+    atomicAdd(c + SAIM_CNT_DECISIONS, (unsigned long long)a.K * a.T * N);
+    atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)cn.flips);
+    atomicAdd(c + SAIM_CNT_ROUNDS, (unsigned long long)cn.rounds);
+    atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)cn.unif);
+    atomicAdd(c + SAIM_CNT_FP64, (unsigned long long)fp64);
+    atomicAdd(c + SAIM_CNT_UNCERTIFIED, (unsigned long long)unc);
+    atomicAdd(c + SAIM_CNT_FEASIBLE, (unsigned long long)nfeas);
+    atomicAdd(c + SAIM_CNT_PHILOX, (unsigned long long)cn.philox);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Launch: grid (ceil(R / wpc), n_inst), wpc warps per CTA.
+typedef void (*qkp_kernel_t)(const RunArgs);
+
+template <int NPL, int QB>
+static qkp_kernel_t pick() { return saim_qkp_kernel<NPL, QB>; }
+
+static qkp_kernel_t qkp_kernel_for(int npl, int qb) {
+#define SAIM_QKP_CASE(P)                                \
+  if (npl <= P) return qb == 1 ? pick<P, 1>() : pick<P, 2>();
+  SAIM_QKP_CASE(1) SAIM_QKP_CASE(2) SAIM_QKP_CASE(3) SAIM_QKP_CASE(4) SAIM_QKP_CASE(6)
+  SAIM_QKP_CASE(8) SAIM_QKP_CASE(10) SAIM_QKP_CASE(12) SAIM_QKP_CASE(16)
+#undef SAIM_QKP_CASE
+  return nullptr;
+}
+
+int qkp_npl_bucket(int npl) {
+  const int b[] = {1, 2, 3, 4, 6, 8, 10, 12, 16};
+  for (int v : b)
+    if (npl <= v) return v;
+  return -1;
+}
+
+// max_wpc: warps per CTA limited by threads (launch bounds), registers and shared memory
+// (blob + per-warp phi).  Sets the kernel's dynamic shared-memory limit accordingly.
+cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *max_wpc) {
+  qkp_kernel_t k = qkp_kernel_for(npl, qb);
+  if (!k) return cudaErrorInvalidValue;
+  cudaFuncAttributes attr;
+  cudaError_t e = cudaFuncGetAttributes(&attr, k);
+  if (e != cudaSuccess) return e;
+  int wpc = attr.maxThreadsPerBlock / 32;
+  if (wpc > 32) wpc = 32;
+  const int per_warp = npl * 32 * 4;
+  const int by_smem = (smem_optin - blob_bytes - (int)attr.sharedSizeBytes - 64) / per_warp;
+  if (by_smem < wpc) wpc = by_smem;
+  if (wpc < 1) return cudaErrorInvalidConfiguration;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, blob_bytes + wpc * per_warp);
+  if (e != cudaSuccess) return e;
+  *max_wpc = wpc;
+  return cudaSuccess;
+}
+
+// Dynamic shared memory = blob + wpc * npl * 32 floats (per-warp phi).
+cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int blob_bytes, cudaStream_t st) {
+  qkp_kernel_t k = qkp_kernel_for(npl, qb);
+  if (!k) return cudaErrorInvalidValue;
+  dim3 grid((a.R + wpc - 1) / wpc, n_inst);
+  k<<<grid, wpc * 32, blob_bytes + wpc * npl * 32 * 4, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace saim
+
+// ---------------------------------------------------------------------------------------------
+// Self-tests (include/saim.h saim_selftest).
+namespace saim {
+__global__ void selftest_philox_kernel(const uint32_t *in, uint32_t *out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t *p = in + 6 * i;
+  const uint4 o = philox4x32_10(make_uint4(p[0], p[1], p[2], p[3]), make_uint2(p[4], p[5]));
+  out[4 * i + 0] = o.x; out[4 * i + 1] = o.y; out[4 * i + 2] = o.z; out[4 * i + 3] = o.w;
+}
+
+__global__ void selftest_logit_kernel(unsigned long long *out) {
+  // one thread per numerator 2m+1, m in [0, 2^23)
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= (1u << 23)) return;
+  const uint32_t w = m << 9;                       // any word with floor(w / 2^9) = m
+  const float lf = logit_f32(w);
+  const double u = uniform_f64(w);
+  const double l = log(u) - log1p(-u);
+  const double err = fabs((double)lf - l);
+  const double rel = err / ((double)kLogitAbs + (double)kLogitRel * fabs(l));
+  atomicMax(out + 0, (unsigned long long)__double_as_longlong(rel));   // non-negative doubles order as ints
+  atomicMax(out + 1, (unsigned long long)__double_as_longlong(err));
+}
+
+int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64) {
+  if (which == 0) {
+    uint32_t *d_in = nullptr, *d_out = nullptr;
+    if (cudaMalloc(&d_in, sizeof(uint32_t) * 6 * (size_t)n) != cudaSuccess) return -1;
+    if (cudaMalloc(&d_out, sizeof(uint32_t) * 4 * (size_t)n) != cudaSuccess) { cudaFree(d_in); return -1; }
+    cudaMemcpy(d_in, in_u32, sizeof(uint32_t) * 6 * (size_t)n, cudaMemcpyHostToDevice);
+    selftest_philox_kernel<<<(n + 127) / 128, 128>>>(d_in, d_out, n);
+    cudaError_t e = cudaMemcpy(out_u32, d_out, sizeof(uint32_t) * 4 * (size_t)n, cudaMemcpyDeviceToHost);
+    cudaFree(d_in); cudaFree(d_out);
+    return e == cudaSuccess ? 0 : -1;
+  }
+  if (which == 1) {
+    unsigned long long *d = nullptr;
+    if (cudaMalloc(&d, 16) != cudaSuccess) return -1;
+    cudaMemset(d, 0, 16);
+    selftest_logit_kernel<<<(1u << 23) / 256, 256>>>(d);
+    unsigned long long h[2];
+    cudaError_t e = cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    memcpy(&out_f64[0], &h[0], 8);
+    memcpy(&out_f64[1], &h[1], 8);
+    return e == cudaSuccess ? 0 : -1;
+  }
+  return -1;
+}
+}  // namespace saim

@@ -1,0 +1,198 @@
+"""GPU <-> oracle parity through the C ABI (marked gpu; run on a B200).
+
+The CUDA path and the oracle (oracle/, plain C) share no code; both receive the same seeded
+inputs (saim_inputs) and must agree BIT-EXACTLY on every integer output: per-iteration samples
+x_k (incl. slack bits), f(x_k), feasibility, residuals r(x_k), Lagrange accumulators Lambda_k,
+per-replica best (f, x, k), feasible counts, and the flip count.  Decisions are the exact real
+predicate on both sides (R18), so no decision may differ; the kernel's `uncertified`
+counter must be 0.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import saim_inputs as si
+from oracle.reference import brute_force_opt
+
+pytestmark = pytest.mark.gpu
+I64MAX = np.iinfo(np.int64).max
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2501_04971_b200 as P
+    from paper_2501_04971_b200 import build
+    build.build()
+    return P
+
+
+def gpu_run(P, Q, c, A, b, Pen, eta, beta_max, seed, R, K, T, rep0=0, trace=True, final=True):
+    import torch
+    sol = P.Solver(Q, c, A, b, Pen, eta, beta_max)
+    out = sol.run(seed, R, K, T, rep0=rep0, trace=trace, final=final)
+    torch.cuda.synchronize()
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    res["counters"] = P.counters_dict(out["counters"])
+    res["info"] = sol.info
+    res["inst"] = [sol.instance(s) for s in range(sol.n_inst)]
+    sol.close()
+    return res
+
+
+def compare(g, o, s, reps, N, K, M):
+    """GPU result g (all replicas of instance s) vs oracle result o for replica indices reps."""
+    WN = (N + 31) // 32
+    reps = np.asarray(reps)
+    gx = g["tr_x"][s, reps].view(np.uint32)
+    assert np.array_equal(gx[..., :WN], o["tr_x"]), "samples x_k differ"
+    assert np.all(gx[..., WN:] == 0)
+    assert np.array_equal(g["tr_f"][s, reps], o["tr_f"])
+    assert np.array_equal(g["tr_feas"][s, reps], o["tr_feas"])
+    if M:
+        assert np.array_equal(g["tr_r"][s, reps], o["tr_r"])
+        assert np.array_equal(g["tr_lam"][s, reps], o["tr_lam"])
+    assert np.array_equal(g["best_f"][s, reps], o["best_f"])
+    assert np.array_equal(g["best_k"][s, reps], o["best_k"])
+    assert np.array_equal(g["best_x"][s, reps].view(np.uint32), o["best_x"])
+    assert np.array_equal(g["n_feasible"][s, reps], o["n_feasible"])
+    if "final_x" in o:
+        assert np.array_equal(g["final_x"][s, reps].view(np.uint32)[..., :WN], o["final_x"])
+        if M:
+            assert np.array_equal(g["final_lam"][s, reps], o["final_lam"])
+
+
+def run_both(P, probs, Pens, eta, beta_max, seed, R, K, T, reps=None, rep0=0):
+    Q, c, A, b = si.stack(probs)
+    g = gpu_run(P, Q, c, A, b, Pens, eta, beta_max, seed, R, K, T, rep0=rep0)
+    assert g["counters"]["uncertified"] == 0
+    flips = 0
+    for s, pr in enumerate(probs):
+        op = oracle.OracleProblem.from_inputs(pr, Pens[s], eta, beta_max, inst=s)
+        assert g["inst"][s]["N"] == op.N and (g["inst"][s]["s_o"], g["inst"][s]["s_c"]) == op.scales()
+        rr = list(range(R)) if reps is None else list(reps)
+        if reps is None:
+            o = op.run(seed, R, K, T, rep0=rep0, trace=True, final=True)
+            flips += o["counters"]["flips"]
+            compare(g, o, s, rr, op.N, K, pr.M)
+        else:
+            for r in rr:                       # sampled replicas, one oracle call each (global index)
+                o = op.run(seed, 1, K, T, rep0=rep0 + r, trace=True, final=True)
+                compare(g, o, s, [r], op.N, K, pr.M)
+    if reps is None:
+        assert g["counters"]["flips"] == flips
+    assert g["counters"]["decisions"] == sum(K * T * R * g["inst"][s]["N"] for s in range(len(probs)))
+    return g
+
+
+# ---------------------------------------------------------------------------------------------
+def test_device_philox_matches_oracle_and_kat(P):
+    rng = np.random.default_rng(0)
+    inp = rng.integers(0, 2 ** 32, size=(500, 6), dtype=np.uint64).astype(np.uint32)
+    inp[0] = 0
+    inp[1] = 0xFFFFFFFF
+    out = P.selftest_philox(inp)
+    for i in range(inp.shape[0]):
+        assert list(out[i]) == oracle.philox(inp[i, :4], inp[i, 4:])
+    assert list(out[0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+
+
+def test_logit_error_bound_exhaustive(P):
+    """The fp32 logit's error over ALL 2^23 uniforms is inside the bound used to certify decisions."""
+    r = P.selftest_logit()
+    assert r["max_ratio"] < 0.5, r
+
+
+def test_parity_config0_full(P):
+    cfg = si.config_instances(0)
+    g = run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T)
+    # Eq. 2 optimum by brute force: every best is >= OPT and inst_best decodes to (f, replica)
+    pr = cfg.instances[0]
+    opt, _ = brute_force_opt(pr.Q, pr.c, pr.A, pr.b)
+    bf = g["best_f"][0][g["best_k"][0] >= 0]
+    assert bf.size and np.all(bf >= opt) and (bf == opt).mean() >= 0.5
+    key = int(g["inst_best"][0])
+    assert key >> 20 == bf.min()
+    rho = key & ((1 << 20) - 1)
+    assert g["best_f"][0][rho] == bf.min() and np.all(g["best_f"][0][:rho] > bf.min())
+
+
+@pytest.mark.parametrize("seed", [2, 0xDEADBEEFCAFEF00D])
+def test_parity_config0_seeds(P, seed):
+    cfg = si.config_instances(0)
+    run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=seed, R=32, K=6, T=50)
+
+
+def _qkp(n, d, seed, cap=None):
+    p = si.qkp(n, d, [77, n, seed])
+    if cap is not None:
+        p.b[:] = cap
+    return p
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 64, 65, 95, 129])
+def test_parity_ragged_sizes(P, n):
+    """Ragged tails: N = n + q spans several 32-spin blocks with a partial last block."""
+    p = _qkp(n, 0.5, 1)
+    run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=3, R=8, K=4, T=30)
+
+
+def test_parity_edge_cases(P):
+    # capacity 1 (one slack bit), T = 1 (fixed beta = beta_max), K = 1
+    p = _qkp(24, 0.5, 2, cap=1)
+    run_both(P, [p], [2.0], 20.0, 10.0, seed=4, R=8, K=1, T=1)
+    run_both(P, [p], [2.0], 20.0, 10.0, seed=4, R=8, K=5, T=1)
+    # eta = 0: penalty-method baseline
+    p = _qkp(40, 0.25, 3)
+    run_both(P, [p], [si.paper_P(p, 2.0)], 0.0, 10.0, seed=5, R=8, K=5, T=40)
+    # linear objective with one constraint (0-1 knapsack), Q = None
+    p = _qkp(50, 0.0, 4)
+    p.Q = None
+    run_both(P, [p], [5.0], 0.05, 50.0, seed=6, R=8, K=5, T=40)
+    # unconstrained (M = 0)
+    q = _qkp(20, 1.0, 5)
+    q.M, q.A, q.b = 0, np.zeros((0, 20), np.int32), np.zeros(0, np.int64)
+    run_both(P, [q], [1.0], 1.0, 5.0, seed=7, R=8, K=3, T=30)
+    # Q entries beyond int8 -> int16 shared-memory storage
+    p = _qkp(45, 0.5, 6)
+    p.Q = (p.Q * 300).astype(np.int32)
+    run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=8, R=8, K=4, T=40)
+    # a high-beta, tiny-field regime (decisions near the sigma boundary exercise the certification)
+    p = _qkp(30, 0.5, 7)
+    run_both(P, [p], [0.01], 0.001, 0.05, seed=9, R=8, K=4, T=50)
+
+
+def test_parity_multi_instance_batch(P):
+    """Instances with different N (different slack counts) in one launch; RNG keyed on instance."""
+    probs = [_qkp(60, 0.5, s, cap=c) for s, c in enumerate([3, 200, 1500, 70000 // 50])]
+    run_both(P, probs, [si.paper_P(p, 2.0) for p in probs], 20.0, 10.0, seed=10, R=16, K=4, T=30)
+
+
+def test_sharding_invariance(P):
+    """RNG keyed on the global replica index: two half-range launches equal one full launch."""
+    cfg = si.config_instances(0)
+    Q, c, A, b = si.stack(cfg.instances)
+    full = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 11, 64, 5, 40)
+    lo = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 11, 32, 5, 40, rep0=0)
+    hi = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 11, 32, 5, 40, rep0=32)
+    for k in ["tr_x", "tr_f", "best_f", "best_x", "final_x"]:
+        assert np.array_equal(full[k][:, :32], lo[k]) and np.array_equal(full[k][:, 32:], hi[k])
+
+
+def test_parity_config1_sampled(P):
+    """BASELINE config 1 at full size (both densities in one launch, the bench's configuration);
+    the oracle recomputes sampled replicas one by one."""
+    cfg = si.config_instances(1)
+    run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
+             reps=[0, 377, 1023])
+
+
+def test_parity_config2_sampled(P):
+    """BASELINE config 2 (headline) at full size; sampled replicas against the oracle."""
+    cfg = si.config_instances(2)
+    run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
+             reps=[0, 4095])
