@@ -33,31 +33,47 @@ namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
 // |logit_f32(u) - logit(u)| <= kLogitAbs + kLogitRel * |logit(u)| for every representable u
-// (checked exhaustively over all 2^23 uniforms by tests/test_gpu_kernels.py).
+// (checked exhaustively over all 2^23 uniforms by tests/test_gpu_parity.py).
 constexpr float kLogitAbs = 0x1p-17f;
 constexpr float kLogitRel = 0x1p-19f;
-// fp32 field: |z_f32 - z| <= kZRel * S with S = |K1 phi| + |A|(|K2 v| + |K3|); the true bound
-// is ~3 * 2^-24 (three roundings + fp32 constants), kZRel leaves a 5x margin.
-constexpr float kZRel = 0x1p-20f;
+// fp32 field: |z_f32 - z| <= 2^-20 * S with S = |K1 phi| + |A|(|K2 v| + |K3|).  The true bound
+// is ~3 * 2^-24 (three roundings plus fp32-rounded constants): a 5x margin.  The saturation test
+// |z| - 2^-20 S > ln(2^24-1) is evaluated as fl(z * (+-2^20) - S) > 2^20 * kSatThr (one FFMA with
+// an immediate; its single rounding costs < 1e-6 of the 7.7e-6 margin built into kSatThr).
+constexpr float kZScale = 1048576.0f;                 // 2^20 = 1 / kZRel
+constexpr float kSatThr20 = kSatThr * 1048576.0f;     // exact (power-of-two scaling)
+// 28 warps x 32 lanes: one CTA of 28 replicas per SM covers 4096 replicas in one wave (<= 72 regs).
+constexpr int kQkpMaxThreads = 896;
 
 __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
   return i == 0 ? u.x : (i == 1 ? u.y : (i == 2 ? u.z : u.w));
 }
 
+__device__ __forceinline__ float lg2_approx(float x) {   // MUFU.LG2; inputs here are normal
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float logit_f32(uint32_t w) {
   const float u = uniform_f32(w);
-  return (__log2f(u) - __log2f(1.0f - u)) * 0.693147180559945309f;
+  return (lg2_approx(u) - lg2_approx(1.0f - u)) * 0.693147180559945309f;
+}
+
+// Lazily drawn uniforms: kept out of line so the compiler cannot hoist the 10-round Philox into
+// the common (saturated) path -- it runs only when some lane of the group needs its u.
+__device__ __noinline__ uint4 philox_group_lazy(uint2 key, int g, int lane, int t, int k, uint32_t srho) {
+  return philox_group(key, g, lane, t, k, srho);
 }
 
 struct Cnt {
-  uint32_t rounds = 0, flips = 0, unif = 0, fp64 = 0, uncert = 0, philox = 0;
+  uint32_t flips = 0, unif = 0, fp64 = 0, uncert = 0, philox = 0;
 };
 
-// fp64 re-evaluation of one decision (R18 slow path).  beta is recomputed exactly as
-// the fast path's constants were derived (beta_max * t / (T-1)).
+// fp64 re-evaluation of one decision (R18 slow path).
 __device__ __noinline__ int decide_fp64(float phib, float v, float A, double beta, double c_o, double c_p,
-                                        double LC, uint32_t w, uint32_t *uncert) {
-  const double K1d = beta * c_o, K2d = beta * c_p, K3d = beta * LC;
+                                        double c_l, long long Lam, uint32_t w, uint32_t *uncert) {
+  const double K1d = beta * c_o, K2d = beta * c_p, K3d = beta * (c_l * (double)Lam);
   const double Ad = (double)A, vd = (double)v, pd = (double)phib;
   const double z = fma(K1d, pd, -(Ad * fma(K2d, vd, K3d)));
   const double S = fabs(K1d * pd) + fabs(Ad) * (fabs(K2d * vd) + fabs(K3d));
@@ -69,15 +85,33 @@ __device__ __noinline__ int decide_fp64(float phib, float v, float A, double bet
   return d > 0.0;
 }
 
+// phi_i -= delta * Q[j][i] for the lane's items i = 32m + lane (one Q row, lane-major).
+template <int NPL, int QB>
+__device__ __forceinline__ void phi_update(const uint32_t *row, float *phw, float dl) {
+  constexpr int E = 4 / QB, QW = (NPL + E - 1) / E;
+  constexpr float kQBias = (float)(1 << (8 * QB - 1));
+#pragma unroll
+  for (int w = 0; w < QW; ++w) {
+    const uint32_t word = row[32 * w];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int m = E * w + e;
+      if (m < NPL) {
+        const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
+        const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
+        phw[32 * m] = fmaf(-dl, q, phw[32 * m]);
+      }
+    }
+  }
+}
+
 }  // namespace
 
 // Shared memory: [instance blob: Q rows | A_ext | c] [phi: warps x NPL*32 floats]
 template <int NPL, int QB>
-__global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
+__global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunArgs a) {
   constexpr int E = 4 / QB;                          // Q entries per 32-bit word
   constexpr int QW = (NPL + E - 1) / E;              // words per lane per Q row
-  constexpr uint32_t kRowBytes = QW * 128u;
-  constexpr float kQBias = (float)(1 << (8 * QB - 1));
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t mbar;
 
@@ -89,17 +123,18 @@ __global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
   if (ridx >= a.R) return;
   const int rho = a.rep0 + ridx;
   const InstHdr H = a.hdr[s];
-  const unsigned char *sQ = smem;
-  const float *sA = reinterpret_cast<const float *>(smem + a.a_off);
+  const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem) + lane;       // Q word (row 0, w 0) of this lane
+  const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane]
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + a.c_off);
   float *phw = reinterpret_cast<float *>(smem + a.blob_bytes) + warp * (NPL * 32) + lane;  // phi[32m + lane]
-  const int n = a.n, N = H.N, NB = (N + 31) >> 5;
+  const int n = a.n, N = H.N, NB = (N + 31) >> 5;    // NB <= NPL + 2 <= 18
+  const int NG = (NB + 3) >> 2;
   const bool has_con = a.M > 0;
 
 #pragma unroll
   for (int m = 0; m < NPL; ++m) phw[32 * m] = (32 * m + lane < n) ? (float)(-sC[32 * m + lane]) : 0.0f;  // x = 0
-  uint64_t xm = 0;                                  // bit b = x_{32b + lane}
-  float r = has_con ? (float)(-H.b0) : 0.0f;        // r = A_ext x - b (exact integer)
+  uint32_t xm = 0;                                  // bit b = x_{32b + lane}
+  float r2 = has_con ? (float)(-2 * H.b0) : 0.0f;   // 2r, r = A_ext x - b (exact integer)
   long long Lam = 0;                                // Lambda_0 = 0 (lambda_0 = 0)
   long long best_f = LLONG_MAX;
   int best_k = -1, nfeas = 0;
@@ -108,96 +143,100 @@ __global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
 
   const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
   const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
+  const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : 0.0;
 
   // Flip of spin j = 32b + L by delta = dl (+1/-1): Eq. 9 in incremental form.
   auto apply_flip = [&](int b, int L, float AL, float dl) {
-    r = fmaf(dl, AL, r);
-    if (lane == L) xm ^= (1ull << b);
+    r2 = fmaf(dl + dl, AL, r2);
+    if (lane == L) xm ^= (1u << b);
     const int j = 32 * b + L;
-    if (j < n) {
-      const uint32_t *row = reinterpret_cast<const uint32_t *>(sQ + (size_t)j * kRowBytes) + lane;
-#pragma unroll
-      for (int w = 0; w < QW; ++w) {
-        const uint32_t word = row[32 * w];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int m = E * w + e;
-          if (m < NPL) {
-            const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
-            const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
-            phw[32 * m] = fmaf(-dl, q, phw[32 * m]);
-          }
-        }
-      }
-    }
+    if (j < n) phi_update<NPL, QB>(sQl + j * (QW * 32), phw, dl);
     ++cn.flips;
   };
 
   for (int k = 0; k < a.K; ++k) {
     const double LC = H.c_l * (double)Lam;           // c_l Lambda = (eta/s_c^2) Lambda
-    for (int t = 0; t < a.T; ++t) {
-      const double beta = (a.T >= 2) ? a.beta_max * (double)t / (double)(a.T - 1) : a.beta_max;
-      const bool bz = (a.T >= 2) && (t == 0);        // beta_0 = 0: x_i = [u < 1/2]
-      const float K1 = (float)(beta * H.c_o), K2 = (float)(beta * H.c_p), K3 = (float)(beta * LC);
-      uint4 uw = make_uint4(0, 0, 0, 0);
-      bool have_u = false;
-      for (int b = 0; b < NB; ++b) {
-        if ((b & 3) == 0) have_u = false;
-        const int nvalid = N - 32 * b;
-        uint32_t pending = nvalid >= 32 ? kFull : ((1u << nvalid) - 1u);
-        const bool valid = lane < nvalid;
-        const float A = valid ? sA[32 * b + lane] : 0.0f;
-        int xb = (int)((xm >> b) & 1ull);
-        if (bz) {
-          if (!have_u) { uw = philox_group(key, b >> 2, lane, t, k, srho); have_u = true; cn.philox += 32; }
-          const int nx = (sel4(uw, b & 3) >> 31) == 0u;   // u < 1/2  <=>  w < 2^31
-          uint32_t fm = __ballot_sync(kFull, valid && nx != xb);
-          cn.unif += __popc(pending);
-          ++cn.rounds;
-          while (fm) {                                      // decisions are state-independent
-            const int L = __ffs(fm) - 1;
-            fm &= fm - 1u;
-            apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
-          }
-          continue;
-        }
-        const float AK2 = A * K2, AK3 = A * K3;
-        const float aAK2 = fabsf(AK2), aAK3 = fabsf(AK3);
-        const bool item_blk = 32 * b < n;
-        for (;;) {
-          ++cn.rounds;
-          const float phib = item_blk ? phw[32 * b] : 0.0f;
-          const float v = fmaf(A, xb ? -1.0f : 1.0f, 2.0f * r);
-          const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));
-          const float S = fmaf(K1, fabsf(phib), fmaf(aAK2, fabsf(v), aAK3));
-          const float e = S * kZRel;
-          const bool mine = (pending >> lane) & 1u;
-          const bool sat = fabsf(z) - e > kSatThr;
-          int nx = z > 0.0f;
-          const uint32_t need = __ballot_sync(kFull, mine && !sat);
-          if (need) {
-            if (!have_u) { uw = philox_group(key, b >> 2, lane, t, k, srho); have_u = true; cn.philox += 32; }
-            cn.unif += __popc(need);
-            if (mine && !sat) {
-              const uint32_t w = sel4(uw, b & 3);
-              const float l = logit_f32(w);
-              const float d = z - l;
-              const float el = kLogitAbs + kLogitRel * fabsf(l);
-              if (fabsf(d) > (e + el) * 1.0001f) {
-                nx = d > 0.0f;
-              } else {
-                ++cn.fp64;
-                nx = decide_fp64(phib, v, A, beta, H.c_o, H.c_p, LC, w, &cn.uncert);
-              }
+    int t0 = 0;
+    if (a.T >= 2) {
+      // ---- sweep t = 0: beta_0 = 0, x_i = [u < 1/2] (state-independent; R3, R5) ----
+      t0 = 1;
+      for (int g = 0; g < NG; ++g) {
+        const uint4 uw = philox_group(key, g, lane, 0, k, srho);
+        cn.philox += 32;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int b = 4 * g + bb;
+          if (b < NB) {
+            const bool valid = lane < N - 32 * b;
+            const int xb = (xm >> b) & 1u;
+            const int nx = (sel4(uw, bb) >> 31) == 0u;   // u < 1/2  <=>  w < 2^31
+            uint32_t fm = __ballot_sync(kFull, valid && nx != xb);
+            cn.unif += __popc(__ballot_sync(kFull, valid));
+            const float A = valid ? sAl[32 * b] : 0.0f;
+            while (fm) {
+              const int L = __ffs(fm) - 1;
+              fm &= fm - 1u;
+              apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
             }
           }
-          const uint32_t fm = __ballot_sync(kFull, mine && nx != xb);
-          if (!fm) break;
-          const int L = __ffs(fm) - 1;
-          apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
-          if (lane == L) xb ^= 1;
-          pending &= ~((2u << L) - 1u);
-          if (!pending) break;
+        }
+      }
+    }
+    for (int t = t0; t < a.T; ++t) {
+      const double beta = (a.T >= 2) ? bstep * (double)t : a.beta_max;
+      const float K1 = (float)(beta * H.c_o), K2 = (float)(beta * H.c_p), K3 = (float)(beta * LC);
+      for (int g = 0; g < NG; ++g) {
+        uint4 uw = make_uint4(0, 0, 0, 0);
+        bool have_u = false;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int b = 4 * g + bb;
+          if (b >= NB) break;
+          const bool valid = lane < N - 32 * b;
+          const float A = valid ? sAl[32 * b] : 0.0f;
+          const bool xb = (xm >> b) & 1u;
+          const float sg = xb ? -1.0f : 1.0f;            // v = 2 r0 + A = 2r + A (1 - 2 x_i)
+          const float sq = xb ? kZScale : -kZScale;       // "quiet" direction: z > 0 keeps x = 1
+          const float AK2 = A * K2, AK3 = A * K3;
+          const bool item_blk = 32 * b < n;
+          float phib = item_blk ? phw[32 * b] : 0.0f;
+          int lo = 0;                                     // lanes >= lo are still pending
+          for (;;) {
+            const float v = fmaf(A, sg, r2);
+            const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));            // beta_t F_i (fp32)
+            const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
+            const bool mine = valid && lane >= lo;
+            // quiet: saturated towards the current value (no flip, no uniform needed)
+            const bool quiet = fmaf(z, sq, -S) > kSatThr20;
+            const uint32_t act = __ballot_sync(kFull, mine && !quiet);
+            if (!act) break;                                                // common case
+            const bool sat = fabsf(z) * kZScale - S > kSatThr20;
+            int nx = z > 0.0f;
+            const uint32_t need = __ballot_sync(kFull, mine && !sat);
+            if (need) {
+              if (!have_u) { uw = philox_group_lazy(key, g, lane, t, k, srho); have_u = true; cn.philox += 32; }
+              cn.unif += __popc(need);
+              if (mine && !sat) {
+                const uint32_t w = sel4(uw, bb);
+                const float l = logit_f32(w);
+                const float d = z - l;
+                const float el = kLogitAbs + kLogitRel * fabsf(l);
+                if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
+                  nx = d > 0.0f;
+                } else {
+                  ++cn.fp64;
+                  nx = decide_fp64(phib, v, A, beta, H.c_o, H.c_p, H.c_l, Lam, w, &cn.uncert);
+                }
+              }
+            }
+            const uint32_t fm = __ballot_sync(kFull, mine && nx != (int)xb);
+            if (!fm) break;
+            const int L = __ffs(fm) - 1;
+            apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+            lo = L + 1;
+            if (lo >= 32) break;
+            phib = item_blk ? phw[32 * b] : 0.0f;
+          }
         }
       }
     }
@@ -205,9 +244,9 @@ __global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
     int fpart = 0, load = 0;
 #pragma unroll
     for (int m = 0; m < NPL; ++m) {
-      if (((xm >> m) & 1ull) && 32 * m + lane < n) {
+      if (((xm >> m) & 1u) && 32 * m + lane < n) {
         fpart += sC[32 * m + lane] - (int)phw[32 * m];      // x_i (c_i - phi_i)
-        load += (int)sA[32 * m + lane];
+        load += (int)sAl[32 * m];
       }
     }
     const long long f = warp_sum_i64((long long)fpart) / 2;  // f = 1/2 sum_i x_i (c_i - phi_i)
@@ -215,10 +254,10 @@ __global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
     const bool feas = !has_con || (long long)load <= H.b0;
     uint32_t myword = 0;
     for (int b = 0; b < NB; ++b) {
-      const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1ull);
+      const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1u);
       if (lane == b) myword = wb;
     }
-    const long long rl = (long long)r;
+    const long long rl = (long long)(0.5f * r2);
     const size_t row = ((size_t)s * a.R + ridx) * a.K + k;
     if (lane == 0) {
       if (a.out.tr_f) a.out.tr_f[row] = f;
@@ -253,7 +292,7 @@ __global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
   if (a.out.final_x) {
     uint32_t myword = 0;
     for (int b = 0; b < NB; ++b) {
-      const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1ull);
+      const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1u);
       if (lane == b) myword = wb;
     }
     if (lane < a.WN) a.out.final_x[ri * a.WN + lane] = myword;
@@ -263,7 +302,6 @@ __global__ void __launch_bounds__(1024, 1) saim_qkp_kernel(const RunArgs a) {
     unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
     atomicAdd(c + SAIM_CNT_DECISIONS, (unsigned long long)a.K * a.T * N);
     atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)cn.flips);
-    atomicAdd(c + SAIM_CNT_ROUNDS, (unsigned long long)cn.rounds);
     atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)cn.unif);
     atomicAdd(c + SAIM_CNT_FP64, (unsigned long long)fp64);
     atomicAdd(c + SAIM_CNT_UNCERTIFIED, (unsigned long long)unc);
