@@ -179,6 +179,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-reference-variant", action="store_true",
+                    help="skip timing the no-early-exit variant")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -216,6 +218,24 @@ def main():
         step(1000 + i)
     torch.cuda.synchronize()
 
+    # Transparency: the same workload with the exact frozen-anneal early exit disabled (every
+    # sweep evaluated); identical outputs (tests/test_gpu_parity.py::test_freeze_exit_is_exact).
+    nofreeze = None
+    if not args.no_reference_variant:
+        sol_nf = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev, flags=P.FLAG_NO_FREEZE_EXIT)
+        out_nf = sol_nf.alloc_outputs(R, cfg.K)
+        sol_nf.run(999, R, cfg.K, cfg.T, rep0=rep0, out=out_nf, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sol_nf.run(1, R, cfg.K, cfg.T, rep0=rep0, out=out_nf, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        t_nf = e0.elapsed_time(e1) / 1e3
+        nofreeze = {"value": R * cfg.K * cfg.T * sum(Ns) * world / t_nf, "unit": "updates/s",
+                    "ms_per_step": 1e3 * t_nf, "counters": P.counters_dict(out_nf["counters"])}
+        sol_nf.close()
+
     # ---- device-timed region: K steps, per-step CUDA events, L2 flush between steps ----
     clocks = ClockSampler(dev)
     if world > 1:
@@ -249,7 +269,9 @@ def main():
 
     # ---- kernel-only time of the dominant kernel (main SAIM kernel; init kernel is ~2 us) ----
     c0 = counters[-1]
-    ops = (c0["decisions"] * OPS_DECISION + c0["uniforms"] * OPS_UNIFORM
+    # evaluated decisions only (sweeps skipped by the exact early exit are not counted as work)
+    evaluated = c0["decisions"] * c0["sweeps"] / float(R * cfg.K * cfg.T * sol.n_inst)
+    ops = (evaluated * OPS_DECISION + c0["uniforms"] * OPS_UNIFORM
            + c0["flips"] * OPS_FLIP_PER_ITEM * n_items)
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     peaks = measured_peaks()
@@ -298,11 +320,13 @@ def main():
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
                          "frac": achieved / peak_ops, "traffic": None,
-                         "ops_per_launch": ops, "ops_model": f"{OPS_DECISION}*decisions + {OPS_UNIFORM}*uniforms + "
+                         "ops_per_launch": ops, "ops_model": f"{OPS_DECISION}*evaluated decisions + {OPS_UNIFORM}*uniforms + "
                                                             f"{OPS_FLIP_PER_ITEM}*n*flips (lane-ops)",
                          "peak_basis": f"{sm_count} SMs x {LANES_PER_SM_CLK} lanes/clk x {sm_mhz:.0f} MHz "
                                        "(measured median SM clock under load)"},
             "counters": c0,
+            "evaluated_sweep_fraction": c0["sweeps"] / float(R * cfg.K * cfg.T * sol.n_inst),
+            "no_freeze_exit": nofreeze,
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},

@@ -41,7 +41,7 @@ extern "C" {
 /* Counters (uint64[SAIM_NUM_COUNTERS]) accumulated by saim_run over all replicas. */
 #define SAIM_CNT_DECISIONS 0     /* attempted p-bit updates = n_inst*R*K*T*N */
 #define SAIM_CNT_FLIPS 1         /* decisions that changed x_i (identical to the oracle's count) */
-#define SAIM_CNT_ROUNDS 2        /* speculative evaluation rounds (warp/group-wide) */
+#define SAIM_CNT_SWEEPS 2        /* sweeps actually evaluated (the rest were certified frozen, see flags) */
 #define SAIM_CNT_UNIFORMS 3      /* decisions for which the uniform u had to be drawn (unsaturated) */
 #define SAIM_CNT_FP64 4          /* decisions re-evaluated on the fp64 slow path */
 #define SAIM_CNT_UNCERTIFIED 5   /* decisions not certified even in fp64 (expected 0) */
@@ -66,8 +66,14 @@ typedef struct {
   double eta;              /* Lagrange step eta >= 0 (Algorithm 1); eta = 0 is the penalty-method baseline */
   double beta_max;         /* final inverse temperature of the linear ramp, > 0 */
   int32_t device;          /* CUDA device ordinal */
-  int32_t flags;           /* reserved, 0 */
+  int32_t flags;           /* SAIM_FLAG_* */
 } saim_params;
+
+/* saim_params.flags.  By default an anneal stops evaluating sweeps once a whole sweep was
+ * certified frozen (every spin saturated towards its current value): the fields are then
+ * constant and beta_t only grows, so all later sweeps of that anneal provably change nothing
+ * (DESIGN.md "Exact early exit").  Results are bit-identical either way. */
+#define SAIM_FLAG_NO_FREEZE_EXIT 1
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),

@@ -18,7 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsaim.so")
 
 SAIM_OK, SAIM_EINVAL, SAIM_ERANGE, SAIM_ESMEM, SAIM_ECUDA, SAIM_EUNSUPPORTED, SAIM_ENOMEM = 0, -1, -2, -3, -4, -5, -6
-COUNTER_NAMES = ["decisions", "flips", "rounds", "uniforms", "fp64", "uncertified", "feasible", "philox"]
+COUNTER_NAMES = ["decisions", "flips", "sweeps", "uniforms", "fp64", "uncertified", "feasible", "philox"]
+FLAG_NO_FREEZE_EXIT = 1
 EXPORTS = ["saim_create", "saim_run", "saim_get_info", "saim_get_instance", "saim_destroy",
            "saim_last_error", "saim_selftest"]
 
@@ -96,7 +97,7 @@ def _arr(x, dtype, shape):
 class Solver:
     """A compiled SAIM problem batch resident on one GPU (saim_create / saim_destroy)."""
 
-    def __init__(self, Q, c, A, b, P, eta: float, beta_max: float, device: int = 0):
+    def __init__(self, Q, c, A, b, P, eta: float, beta_max: float, device: int = 0, flags: int = 0):
         lib = load_library()
         c = np.asarray(c)
         if c.ndim == 1:
@@ -112,7 +113,7 @@ class Solver:
         prob = _Problem(S, n, M, None if self._Q is None else self._Q.ctypes.data, self._c.ctypes.data,
                         None if self._A is None else self._A.ctypes.data,
                         None if self._b is None else self._b.ctypes.data)
-        par = _Params(self._P.ctypes.data, float(eta), float(beta_max), int(device), 0)
+        par = _Params(self._P.ctypes.data, float(eta), float(beta_max), int(device), int(flags))
         h = C.c_void_p()
         _check(lib.saim_create(C.byref(prob), C.byref(par), C.byref(h)))
         self._h = h
@@ -123,11 +124,11 @@ class Solver:
         self.n_inst, self.n, self.M = S, n, M
 
     @classmethod
-    def from_config(cls, cfg, device: int = 0):
+    def from_config(cls, cfg, device: int = 0, flags: int = 0):
         """Build from a saim_inputs.Config (all its instances in one batch)."""
         import saim_inputs as si
         Q, c, A, b = si.stack(cfg.instances)
-        return cls(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=device)
+        return cls(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=device, flags=flags)
 
     def instance(self, s: int):
         N = C.c_int32()

@@ -57,6 +57,7 @@ struct saim_ctx {
   int smem_bytes = 0, max_wpc = 32, sm_count = 148;
   uint32_t blob_bytes = 0, a_off = 0, c_off = 0, x_off = 0;
   double beta_max = 0, eta = 0;
+  int flags = 0;
   long long r_abs_max = 0;
   unsigned char *d_blob = nullptr;
   InstHdr *d_hdr = nullptr;
@@ -100,6 +101,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
   ctx->device = par->device;
   ctx->n_inst = S; ctx->n = n; ctx->M = M;
   ctx->beta_max = par->beta_max; ctx->eta = par->eta;
+  ctx->flags = par->flags;
   ctx->hdr.resize(S);
   ctx->q.resize(S);
 
@@ -305,6 +307,7 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
   a.Wn = (ctx->n + 31) / 32; a.WN = (ctx->N_max + 31) / 32;
   a.R = R; a.rep0 = rep0; a.K = K; a.T = T;
   a.seed = seed; a.beta_max = ctx->beta_max;
+  a.flags = ctx->flags;
   a.out = *out;
 
   saim_init_outputs<<<(ctx->n_inst + 255) / 256, 256, 0, st>>>(out->inst_best, ctx->n_inst, out->counters);

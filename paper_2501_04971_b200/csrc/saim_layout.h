@@ -46,6 +46,7 @@ struct RunArgs {
   int32_t n, M;               // items, constraints
   int32_t Wn, WN;             // ceil(n/32), ceil(N_max/32)
   int32_t R, rep0, K, T;
+  int32_t flags;              // saim_params.flags
   uint64_t seed;
   double beta_max;
   saim_outputs out;           // device pointers

@@ -66,14 +66,29 @@ __device__ __noinline__ uint4 philox_group_lazy(uint2 key, int g, int lane, int 
   return philox_group(key, g, lane, t, k, srho);
 }
 
-struct Cnt {
-  uint32_t flips = 0, unif = 0, fp64 = 0, uncert = 0, philox = 0;
+// Per-warp cold state in shared memory (kept out of the register file: the hot loop runs at
+// 28 warps/SM, i.e. <= 72 registers per thread).
+struct WarpState {
+  double k1step, k2step, k3step;   // beta_t = t * bstep:  K1 = t*bstep*c_o, K2 = t*bstep*c_p, K3 = t*bstep*c_l*Lambda
+  double bstep;                    // beta_max / (T-1)   (or beta_max with t := 1 when T == 1)
+  long long Lam;                   // Lambda_k (Lambda_0 = 0)
+  long long best_f;
+  int best_k, nfeas;
+  uint32_t cnt[6];                 // flips, uniforms, fp64, uncertified, philox, sweeps evaluated
+  uint32_t best_word[32];
 };
+enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps };
 
-// fp64 re-evaluation of one decision (R18 slow path).
-__device__ __noinline__ int decide_fp64(float phib, float v, float A, double beta, double c_o, double c_p,
-                                        double c_l, long long Lam, uint32_t w, uint32_t *uncert) {
-  const double K1d = beta * c_o, K2d = beta * c_p, K3d = beta * (c_l * (double)Lam);
+__device__ __forceinline__ void cnt_add(WarpState *ws, int i, uint32_t v) {
+  if ((threadIdx.x & 31) == 0) ws->cnt[i] += v;      // warp-uniform events, counted once
+}
+
+// fp64 re-evaluation of one decision (R18 slow path).  Constants are re-derived in
+// fp64 from the instance header; the bound 2^-47 (S + 1 + |l|) covers their few-ulp roundings.
+__device__ __noinline__ int decide_fp64(float phib, float v, float A, int t, const InstHdr *H, const WarpState *ws,
+                                        uint32_t w) {
+  const double beta = ws->bstep * (double)t;
+  const double K1d = beta * H->c_o, K2d = beta * H->c_p, K3d = beta * (H->c_l * (double)ws->Lam);
   const double Ad = (double)A, vd = (double)v, pd = (double)phib;
   const double z = fma(K1d, pd, -(Ad * fma(K2d, vd, K3d)));
   const double S = fabs(K1d * pd) + fabs(Ad) * (fabs(K2d * vd) + fabs(K3d));
@@ -81,8 +96,7 @@ __device__ __noinline__ int decide_fp64(float phib, float v, float A, double bet
   const double l = log(u) - log1p(-u);
   const double d = z - l;
   const double e = (S + 1.0 + fabs(l)) * 0x1p-47;
-  if (fabs(d) <= e) ++*uncert;
-  return d > 0.0;
+  return (d > 0.0 ? 1 : 0) | (fabs(d) <= e ? 2 : 0);
 }
 
 // phi_i -= delta * Q[j][i] for the lane's items i = 32m + lane (one Q row, lane-major).
@@ -107,7 +121,12 @@ __device__ __forceinline__ void phi_update(const uint32_t *row, float *phw, floa
 
 }  // namespace
 
-// Shared memory: [instance blob: Q rows | A_ext | c] [phi: warps x NPL*32 floats]
+template <int NPL>
+__host__ __device__ constexpr int qkp_warp_smem_bytes() {
+  return ((NPL + 2) * 32 * 4 + (int)sizeof(WarpState) + 15) & ~15;
+}
+
+// Shared memory: [instance blob: Q rows | A_ext | c] [per warp: phi (NPL+2)*32 floats | WarpState]
 template <int NPL, int QB>
 __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunArgs a) {
   constexpr int E = 4 / QB;                          // Q entries per 32-bit word
@@ -121,29 +140,39 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ridx = blockIdx.x * (blockDim.x >> 5) + warp;
   if (ridx >= a.R) return;
-  const int rho = a.rep0 + ridx;
-  const InstHdr H = a.hdr[s];
+  const InstHdr *Hp = a.hdr + s;
   const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem) + lane;       // Q word (row 0, w 0) of this lane
-  const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane]
+  const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane] (0-padded)
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + a.c_off);
-  float *phw = reinterpret_cast<float *>(smem + a.blob_bytes) + warp * (NPL * 32) + lane;  // phi[32m + lane]
-  const int n = a.n, N = H.N, NB = (N + 31) >> 5;    // NB <= NPL + 2 <= 18
-  const int NG = (NB + 3) >> 2;
+  unsigned char *wbase = smem + a.blob_bytes + warp * qkp_warp_smem_bytes<NPL>();
+  float *phw = reinterpret_cast<float *>(wbase) + lane;                        // phi[32b + lane], 0 beyond items
+  WarpState *ws = reinterpret_cast<WarpState *>(wbase + (NPL + 2) * 32 * 4);
+  const int n = a.n;
+  const int N = Hp->N;
+  const int NB = (N + 31) >> 5;                      // NB <= NPL + 2
   const bool has_con = a.M > 0;
 
 #pragma unroll
-  for (int m = 0; m < NPL; ++m) phw[32 * m] = (32 * m + lane < n) ? (float)(-sC[32 * m + lane]) : 0.0f;  // x = 0
+  for (int m = 0; m < NPL + 2; ++m) phw[32 * m] = (32 * m + lane < n) ? (float)(-sC[32 * m + lane]) : 0.0f;  // x = 0
+  if (lane == 0) {
+    ws->bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
+    ws->k1step = ws->bstep * Hp->c_o;
+    ws->k2step = ws->bstep * Hp->c_p;
+    ws->k3step = 0.0;
+    ws->Lam = 0;
+    ws->best_f = LLONG_MAX;
+    ws->best_k = -1;
+    ws->nfeas = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ws->cnt[i] = 0;
+  }
+  ws->best_word[lane] = 0;
+  __syncwarp();
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
-  float r2 = has_con ? (float)(-2 * H.b0) : 0.0f;   // 2r, r = A_ext x - b (exact integer)
-  long long Lam = 0;                                // Lambda_0 = 0 (lambda_0 = 0)
-  long long best_f = LLONG_MAX;
-  int best_k = -1, nfeas = 0;
-  uint32_t best_word = 0;
-  Cnt cn;
+  float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
   const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
-  const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
-  const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : 0.0;
+  const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)(a.rep0 + ridx);
 
   // Flip of spin j = 32b + L by delta = dl (+1/-1): Eq. 9 in incremental form.
   auto apply_flip = [&](int b, int L, float AL, float dl) {
@@ -151,18 +180,17 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (lane == L) xm ^= (1u << b);
     const int j = 32 * b + L;
     if (j < n) phi_update<NPL, QB>(sQl + j * (QW * 32), phw, dl);
-    ++cn.flips;
+    cnt_add(ws, kCntFlips, 1);
   };
 
   for (int k = 0; k < a.K; ++k) {
-    const double LC = H.c_l * (double)Lam;           // c_l Lambda = (eta/s_c^2) Lambda
     int t0 = 0;
     if (a.T >= 2) {
       // ---- sweep t = 0: beta_0 = 0, x_i = [u < 1/2] (state-independent; R3, R5) ----
       t0 = 1;
-      for (int g = 0; g < NG; ++g) {
+      for (int g = 0; 4 * g < NB; ++g) {
         const uint4 uw = philox_group(key, g, lane, 0, k, srho);
-        cn.philox += 32;
+        cnt_add(ws, kCntPhilox, 32);
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
           const int b = 4 * g + bb;
@@ -171,8 +199,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             const int xb = (xm >> b) & 1u;
             const int nx = (sel4(uw, bb) >> 31) == 0u;   // u < 1/2  <=>  w < 2^31
             uint32_t fm = __ballot_sync(kFull, valid && nx != xb);
-            cn.unif += __popc(__ballot_sync(kFull, valid));
-            const float A = valid ? sAl[32 * b] : 0.0f;
+            cnt_add(ws, kCntUnif, __popc(__ballot_sync(kFull, valid)));
+            const float A = sAl[32 * b];
             while (fm) {
               const int L = __ffs(fm) - 1;
               fm &= fm - 1u;
@@ -182,40 +210,46 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         }
       }
     }
+    const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
     for (int t = t0; t < a.T; ++t) {
-      const double beta = (a.T >= 2) ? bstep * (double)t : a.beta_max;
-      const float K1 = (float)(beta * H.c_o), K2 = (float)(beta * H.c_p), K3 = (float)(beta * LC);
-      for (int g = 0; g < NG; ++g) {
+      const double tt = (a.T >= 2) ? (double)t : 1.0;
+      bool active = false;                            // any non-quiet lane in this sweep?
+      const float K1 = (float)(tt * ws->k1step), K2 = (float)(tt * ws->k2step), K3 = (float)(tt * ws->k3step);
+      for (int g = 0; 4 * g < NB; ++g) {
         uint4 uw = make_uint4(0, 0, 0, 0);
         bool have_u = false;
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
           const int b = 4 * g + bb;
           if (b >= NB) break;
-          const bool valid = lane < N - 32 * b;
-          const float A = valid ? sAl[32 * b] : 0.0f;
+          const int hi = N - 32 * b;                      // lanes < hi hold a spin
+          const float A = sAl[32 * b];
           const bool xb = (xm >> b) & 1u;
           const float sg = xb ? -1.0f : 1.0f;            // v = 2 r0 + A = 2r + A (1 - 2 x_i)
           const float sq = xb ? kZScale : -kZScale;       // "quiet" direction: z > 0 keeps x = 1
           const float AK2 = A * K2, AK3 = A * K3;
-          const bool item_blk = 32 * b < n;
-          float phib = item_blk ? phw[32 * b] : 0.0f;
-          int lo = 0;                                     // lanes >= lo are still pending
+          float phib = phw[32 * b];
+          int lo = 0;                                     // lanes in [lo, hi) are still pending
           for (;;) {
             const float v = fmaf(A, sg, r2);
             const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));            // beta_t F_i (fp32)
             const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
-            const bool mine = valid && lane >= lo;
+            const bool mine = lane >= lo && lane < hi;
             // quiet: saturated towards the current value (no flip, no uniform needed)
             const bool quiet = fmaf(z, sq, -S) > kSatThr20;
             const uint32_t act = __ballot_sync(kFull, mine && !quiet);
             if (!act) break;                                                // common case
+            active = true;
             const bool sat = fabsf(z) * kZScale - S > kSatThr20;
             int nx = z > 0.0f;
             const uint32_t need = __ballot_sync(kFull, mine && !sat);
             if (need) {
-              if (!have_u) { uw = philox_group_lazy(key, g, lane, t, k, srho); have_u = true; cn.philox += 32; }
-              cn.unif += __popc(need);
+              if (!have_u) {
+                uw = philox_group_lazy(key, g, lane, t, k, srho);
+                have_u = true;
+                cnt_add(ws, kCntPhilox, 32);
+              }
+              cnt_add(ws, kCntUnif, __popc(need));
               if (mine && !sat) {
                 const uint32_t w = sel4(uw, bb);
                 const float l = logit_f32(w);
@@ -224,8 +258,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
                 if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
                   nx = d > 0.0f;
                 } else {
-                  ++cn.fp64;
-                  nx = decide_fp64(phib, v, A, beta, H.c_o, H.c_p, H.c_l, Lam, w, &cn.uncert);
+                  const int rs = decide_fp64(phib, v, A, a.T >= 2 ? t : 1, Hp, ws, w);
+                  nx = rs & 1;
+                  atomicAdd(&ws->cnt[kCntFp64], 1u);
+                  if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
                 }
               }
             }
@@ -234,11 +270,16 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             const int L = __ffs(fm) - 1;
             apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
             lo = L + 1;
-            if (lo >= 32) break;
-            phib = item_blk ? phw[32 * b] : 0.0f;
+            if (lo >= hi) break;
+            phib = phw[32 * b];
           }
         }
       }
+      cnt_add(ws, kCntSweeps, 1);
+      // Frozen anneal: a sweep in which every spin was certified
+      // saturated towards its current value changed nothing; fields stay constant and beta only
+      // grows, so every later sweep of this anneal is certified the same way -- x_k is final.
+      if (!active && freeze_exit && a.T >= 2) break;
     }
     // ---- readout of x_k (Algorithm 1 "store feasible") ----
     int fpart = 0, load = 0;
@@ -251,13 +292,14 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     }
     const long long f = warp_sum_i64((long long)fpart) / 2;  // f = 1/2 sum_i x_i (c_i - phi_i)
     load = __reduce_add_sync(kFull, load);
-    const bool feas = !has_con || (long long)load <= H.b0;
+    const bool feas = !has_con || (long long)load <= Hp->b0;
     uint32_t myword = 0;
     for (int b = 0; b < NB; ++b) {
       const uint32_t wb = __ballot_sync(kFull, (xm >> b) & 1u);
       if (lane == b) myword = wb;
     }
     const long long rl = (long long)(0.5f * r2);
+    const long long Lam = ws->Lam;
     const size_t row = ((size_t)s * a.R + ridx) * a.K + k;
     if (lane == 0) {
       if (a.out.tr_f) a.out.tr_f[row] = f;
@@ -267,28 +309,37 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     }
     if (a.out.tr_x && lane < a.WN) a.out.tr_x[row * a.WN + lane] = myword;
     if (feas) {
-      ++nfeas;
-      if (f < best_f) {
-        best_f = f;
-        best_k = k;
+      const bool better = f < ws->best_f;
+      if (better) {
         const int rem = n - 32 * lane;
-        best_word = rem >= 32 ? myword : (rem > 0 ? (myword & ((1u << rem) - 1u)) : 0u);
+        ws->best_word[lane] = rem >= 32 ? myword : (rem > 0 ? (myword & ((1u << rem) - 1u)) : 0u);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ws->nfeas += 1;
+        if (better) { ws->best_f = f; ws->best_k = k; }
       }
     }
-    Lam += rl;                                               // lambda_{k+1} = lambda_k + eta g(x_k)
+    __syncwarp();
+    if (lane == 0) {                                  // lambda_{k+1} = lambda_k + eta g(x_k)  (R10)
+      ws->Lam = Lam + rl;
+      ws->k3step = ws->bstep * (Hp->c_l * (double)(Lam + rl));
+    }
+    __syncwarp();
   }
 
   // ---- outputs ----
   const size_t ri = (size_t)s * a.R + ridx;
+  const int rho = a.rep0 + ridx;
   if (lane == 0) {
-    a.out.best_f[ri] = best_f;
-    a.out.best_k[ri] = best_k;
-    a.out.n_feasible[ri] = nfeas;
-    if (best_k >= 0 && a.out.inst_best)
-      atomicMin(reinterpret_cast<long long *>(a.out.inst_best) + s, (best_f << 20) | (long long)rho);
-    if (has_con && a.out.final_lam) a.out.final_lam[ri] = Lam;
+    a.out.best_f[ri] = ws->best_f;
+    a.out.best_k[ri] = ws->best_k;
+    a.out.n_feasible[ri] = ws->nfeas;
+    if (ws->best_k >= 0 && a.out.inst_best)
+      atomicMin(reinterpret_cast<long long *>(a.out.inst_best) + s, (ws->best_f << 20) | (long long)rho);
+    if (has_con && a.out.final_lam) a.out.final_lam[ri] = ws->Lam;
   }
-  if (lane < a.Wn) a.out.best_x[ri * a.Wn + lane] = best_word;
+  if (lane < a.Wn) a.out.best_x[ri * a.Wn + lane] = ws->best_word[lane];
   if (a.out.final_x) {
     uint32_t myword = 0;
     for (int b = 0; b < NB; ++b) {
@@ -297,16 +348,16 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     }
     if (lane < a.WN) a.out.final_x[ri * a.WN + lane] = myword;
   }
-  const uint32_t fp64 = __reduce_add_sync(kFull, cn.fp64), unc = __reduce_add_sync(kFull, cn.uncert);
   if (lane == 0 && a.out.counters) {
     unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
     atomicAdd(c + SAIM_CNT_DECISIONS, (unsigned long long)a.K * a.T * N);
-    atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)cn.flips);
-    atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)cn.unif);
-    atomicAdd(c + SAIM_CNT_FP64, (unsigned long long)fp64);
-    atomicAdd(c + SAIM_CNT_UNCERTIFIED, (unsigned long long)unc);
-    atomicAdd(c + SAIM_CNT_FEASIBLE, (unsigned long long)nfeas);
-    atomicAdd(c + SAIM_CNT_PHILOX, (unsigned long long)cn.philox);
+    atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)ws->cnt[kCntFlips]);
+    atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)ws->cnt[kCntUnif]);
+    atomicAdd(c + SAIM_CNT_FP64, (unsigned long long)ws->cnt[kCntFp64]);
+    atomicAdd(c + SAIM_CNT_UNCERTIFIED, (unsigned long long)ws->cnt[kCntUncert]);
+    atomicAdd(c + SAIM_CNT_FEASIBLE, (unsigned long long)ws->nfeas);
+    atomicAdd(c + SAIM_CNT_PHILOX, (unsigned long long)ws->cnt[kCntPhilox]);
+    atomicAdd(c + SAIM_CNT_SWEEPS, (unsigned long long)ws->cnt[kCntSweeps] + (a.T >= 2 ? (unsigned long long)a.K : 0ull));
   }
 }
 
@@ -326,6 +377,16 @@ static qkp_kernel_t qkp_kernel_for(int npl, int qb) {
   return nullptr;
 }
 
+static int qkp_warp_bytes(int npl) {
+  switch (npl) {
+    case 1: return qkp_warp_smem_bytes<1>();   case 2: return qkp_warp_smem_bytes<2>();
+    case 3: return qkp_warp_smem_bytes<3>();   case 4: return qkp_warp_smem_bytes<4>();
+    case 6: return qkp_warp_smem_bytes<6>();   case 8: return qkp_warp_smem_bytes<8>();
+    case 10: return qkp_warp_smem_bytes<10>(); case 12: return qkp_warp_smem_bytes<12>();
+    default: return qkp_warp_smem_bytes<16>();
+  }
+}
+
 int qkp_npl_bucket(int npl) {
   const int b[] = {1, 2, 3, 4, 6, 8, 10, 12, 16};
   for (int v : b)
@@ -343,7 +404,7 @@ cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *
   if (e != cudaSuccess) return e;
   int wpc = attr.maxThreadsPerBlock / 32;
   if (wpc > 32) wpc = 32;
-  const int per_warp = npl * 32 * 4;
+  const int per_warp = qkp_warp_bytes(npl);
   const int by_smem = (smem_optin - blob_bytes - (int)attr.sharedSizeBytes - 64) / per_warp;
   if (by_smem < wpc) wpc = by_smem;
   if (wpc < 1) return cudaErrorInvalidConfiguration;
@@ -353,12 +414,12 @@ cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *
   return cudaSuccess;
 }
 
-// Dynamic shared memory = blob + wpc * npl * 32 floats (per-warp phi).
+// Dynamic shared memory = blob + wpc * per-warp region (phi + WarpState).
 cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int blob_bytes, cudaStream_t st) {
   qkp_kernel_t k = qkp_kernel_for(npl, qb);
   if (!k) return cudaErrorInvalidValue;
   dim3 grid((a.R + wpc - 1) / wpc, n_inst);
-  k<<<grid, wpc * 32, blob_bytes + wpc * npl * 32 * 4, st>>>(a);
+  k<<<grid, wpc * 32, blob_bytes + wpc * qkp_warp_bytes(npl), st>>>(a);
   return cudaGetLastError();
 }
 

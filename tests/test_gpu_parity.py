@@ -31,9 +31,9 @@ def P():
     return P
 
 
-def gpu_run(P, Q, c, A, b, Pen, eta, beta_max, seed, R, K, T, rep0=0, trace=True, final=True):
+def gpu_run(P, Q, c, A, b, Pen, eta, beta_max, seed, R, K, T, rep0=0, trace=True, final=True, flags=0):
     import torch
-    sol = P.Solver(Q, c, A, b, Pen, eta, beta_max)
+    sol = P.Solver(Q, c, A, b, Pen, eta, beta_max, flags=flags)
     out = sol.run(seed, R, K, T, rep0=rep0, trace=trace, final=final)
     torch.cuda.synchronize()
     res = {k: v.cpu().numpy() for k, v in out.items()}
@@ -196,3 +196,21 @@ def test_parity_config2_sampled(P):
     cfg = si.config_instances(2)
     run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
              reps=[0, 4095])
+
+
+@pytest.mark.parametrize("cfg_idx", [0, 1])
+def test_freeze_exit_is_exact(P, cfg_idx):
+    """Stopping an anneal after a fully certified-frozen sweep
+    gives bit-identical outputs to evaluating every sweep."""
+    cfg = si.config_instances(cfg_idx)
+    Q, c, A, b = si.stack(cfg.instances)
+    R, K = (64, cfg.K) if cfg_idx == 0 else (256, 10)
+    on = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 5, R, K, cfg.T)
+    off = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 5, R, K, cfg.T, flags=P.FLAG_NO_FREEZE_EXIT)
+    for k in ["tr_x", "tr_f", "tr_feas", "tr_r", "tr_lam", "best_f", "best_k", "best_x", "n_feasible",
+              "final_x", "final_lam", "inst_best"]:
+        assert np.array_equal(on[k], off[k]), k
+    for k in ["decisions", "flips", "uniforms", "feasible", "uncertified"]:
+        assert on["counters"][k] == off["counters"][k], k
+    assert off["counters"]["sweeps"] == R * K * cfg.T * len(cfg.instances)
+    assert on["counters"]["sweeps"] <= off["counters"]["sweeps"]
