@@ -162,6 +162,15 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     h.c_o = 1.0 / (double)so;
     h.c_p = P / ((double)sc * (double)sc);
     h.c_l = par->eta / ((double)sc * (double)sc);
+    h.phi_bound = (double)phi_bound;
+    {
+      long long amax = 0;
+      for (int k = 0; k < M; ++k) {
+        amax = std::max(amax, (1LL << (ctx->q[s][k] - 1)));
+        for (int j = 0; j < n; ++j) amax = std::max(amax, (long long)A[(size_t)k * n + j]);
+      }
+      h.v_bound = 2.0 * (double)rmax + (double)amax;
+    }
     ctx->N_max = std::max(ctx->N_max, h.N);
     ctx->n_slack_max = std::max(ctx->n_slack_max, n_slack);
     // exactness proofs (DESIGN.md Appendix B)

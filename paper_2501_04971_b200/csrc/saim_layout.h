@@ -36,6 +36,8 @@ struct InstHdr {
   int64_t s_o, s_c;
   int32_t slack_off;  // MKP: offset of this instance's slack table (entries), unused by QKP
   int32_t pad;
+  double phi_bound;   // max_i |c_i| + sum_j |Q_ij|  >= |phi_i| for every state (host-proven)
+  double v_bound;     // 2 max|r| + max A_ext      >= |2 r0 + A_i| for every state
 };
 
 struct RunArgs {

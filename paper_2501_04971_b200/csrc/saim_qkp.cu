@@ -71,6 +71,7 @@ __device__ __noinline__ uint4 philox_group_lazy(uint2 key, int g, int lane, int 
 struct WarpState {
   double k1step, k2step, k3step;   // beta_t = t * bstep:  K1 = t*bstep*c_o, K2 = t*bstep*c_p, K3 = t*bstep*c_l*Lambda
   double bstep;                    // beta_max / (T-1)   (or beta_max with t := 1 when T == 1)
+  double e0step, e1step;           // scan error bound per unit beta_t: e(A) = t*(e0step + e1step*A)
   long long Lam;                   // Lambda_k (Lambda_0 = 0)
   long long best_f;
   int best_k, nfeas;
@@ -159,6 +160,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     ws->k1step = ws->bstep * Hp->c_o;
     ws->k2step = ws->bstep * Hp->c_p;
     ws->k3step = 0.0;
+    ws->e0step = ws->bstep * Hp->c_o * Hp->phi_bound * 0x1p-20;
+    ws->e1step = ws->bstep * Hp->c_p * Hp->v_bound * 0x1p-20;
     ws->Lam = 0;
     ws->best_f = LLONG_MAX;
     ws->best_k = -1;
@@ -215,31 +218,33 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       const double tt = (a.T >= 2) ? (double)t : 1.0;
       bool active = false;                            // any non-quiet lane in this sweep?
       const float K1 = (float)(tt * ws->k1step), K2 = (float)(tt * ws->k2step), K3 = (float)(tt * ws->k3step);
+      // Scan threshold: quiet <=> +-z_f32 > kSatThr + tt*(e0step + e1step*A), where the second term
+      // bounds |z_f32 - z| for every reachable state (phi_bound, v_bound; 4x margin over 3*2^-24).
+      const float B0 = kSatThr + (float)(tt * ws->e0step) * 1.0001f;
+      const float B1 = (float)(tt * ws->e1step) * 1.0001f;
       for (int g = 0; 4 * g < NB; ++g) {
         uint4 uw = make_uint4(0, 0, 0, 0);
         bool have_u = false;
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          const int b = 4 * g + bb;
-          if (b >= NB) break;
+        const int nbg = min(4, NB - 4 * g);               // blocks in this group
+
+        // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
+        // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
+        // Returns true if a spin of the block flipped.
+        auto process_block = [&](int b, int bb) -> bool {
           const int hi = N - 32 * b;                      // lanes < hi hold a spin
           const float A = sAl[32 * b];
           const bool xb = (xm >> b) & 1u;
           const float sg = xb ? -1.0f : 1.0f;            // v = 2 r0 + A = 2r + A (1 - 2 x_i)
           const float sq = xb ? kZScale : -kZScale;       // "quiet" direction: z > 0 keeps x = 1
           const float AK2 = A * K2, AK3 = A * K3;
-          float phib = phw[32 * b];
+          bool flipped = false;
           int lo = 0;                                     // lanes in [lo, hi) are still pending
           for (;;) {
+            const float phib = phw[32 * b];
             const float v = fmaf(A, sg, r2);
             const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));            // beta_t F_i (fp32)
             const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
             const bool mine = lane >= lo && lane < hi;
-            // quiet: saturated towards the current value (no flip, no uniform needed)
-            const bool quiet = fmaf(z, sq, -S) > kSatThr20;
-            const uint32_t act = __ballot_sync(kFull, mine && !quiet);
-            if (!act) break;                                                // common case
-            active = true;
             const bool sat = fabsf(z) * kZScale - S > kSatThr20;
             int nx = z > 0.0f;
             const uint32_t need = __ballot_sync(kFull, mine && !sat);
@@ -269,10 +274,53 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             if (!fm) break;
             const int L = __ffs(fm) - 1;
             apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+            flipped = true;
             lo = L + 1;
             if (lo >= hi) break;
-            phib = phw[32 * b];
+            (void)sq;
           }
+          return flipped;
+        };
+
+        int bstart = 0;
+        for (;;) {
+          // Speculative scan of blocks bstart..nbg-1 on the current state: bit bb of nq is set if
+          // this lane's spin in block bb is not certified quiet (saturated towards its value).
+          // zz = +-z (sign of the current x): quiet <=> zz > B0 + B1*A (see B0, B1 above).
+          uint32_t nq = 0;
+          auto scan_one = [&](int b, int bb, bool check_valid) {
+            const float A = sAl[32 * b];
+            const float ph = phw[32 * b];
+            const bool xb = (xm >> b) & 1u;
+            const float Asg = xb ? A : -A;                 // -(A (1 - 2x_i))
+            const float v = r2 - Asg;                      // 2 r0 + A
+            const float tq = fmaf(K2, v, K3);
+            const float zz = fmaf(xb ? K1 : -K1, ph, -(Asg * tq));   // (2x_i - 1) * z
+            const bool quiet = zz > fmaf(B1, A, B0);
+            if (!quiet && (!check_valid || lane < N - 32 * b)) nq |= 1u << bb;
+          };
+          if (bstart == 0 && 32 * (4 * g + 4) <= N) {      // hot path: four full blocks
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) scan_one(4 * g + bb, bb, false);
+          } else {
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb)
+              if (bb >= bstart && bb < nbg) scan_one(4 * g + bb, bb, true);
+          }
+          uint32_t m = __reduce_or_sync(kFull, nq);
+          if (!m) break;                                  // common case: the group is quiet
+          active = true;
+          bool flipped = false;
+          while (m) {                                     // active blocks, in order
+            const int bb = __ffs(m) - 1;
+            m &= m - 1u;
+            if (process_block(4 * g + bb, bb)) {          // a flip invalidates the later speculation
+              flipped = true;
+              bstart = bb + 1;
+              break;
+            }
+          }
+          if (!flipped || bstart >= nbg) break;
         }
       }
       cnt_add(ws, kCntSweeps, 1);
@@ -324,6 +372,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (lane == 0) {                                  // lambda_{k+1} = lambda_k + eta g(x_k)  (R10)
       ws->Lam = Lam + rl;
       ws->k3step = ws->bstep * (Hp->c_l * (double)(Lam + rl));
+      ws->e1step = ws->bstep * (Hp->c_p * Hp->v_bound + Hp->c_l * fabs((double)(Lam + rl))) * 0x1p-20;
     }
     __syncwarp();
   }
