@@ -222,10 +222,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // bounds |z_f32 - z| for every reachable state (phi_bound, v_bound; 4x margin over 3*2^-24).
       const float B0 = kSatThr + (float)(tt * ws->e0step) * 1.0001f;
       const float B1 = (float)(tt * ws->e1step) * 1.0001f;
-      for (int g = 0; 4 * g < NB; ++g) {
-        uint4 uw = make_uint4(0, 0, 0, 0);
-        bool have_u = false;
-        const int nbg = min(4, NB - 4 * g);               // blocks in this group
+      int g = 0;                                          // current 128-spin group (4 blocks)
+      int nbg = 4;                                        // blocks in group g
+      uint4 uw = make_uint4(0, 0, 0, 0);                  // group g's uniforms, drawn lazily
+      bool have_u = false;
 
         // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
         // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
@@ -282,47 +282,60 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           return flipped;
         };
 
-        int bstart = 0;
-        for (;;) {
-          // Speculative scan of blocks bstart..nbg-1 on the current state: bit bb of nq is set if
-          // this lane's spin in block bb is not certified quiet (saturated towards its value).
-          // zz = +-z (sign of the current x): quiet <=> zz > B0 + B1*A (see B0, B1 above).
+        // Speculative scan of group g's blocks bb >= bstart on the current state: bit bb of the
+        // result is set if this lane's spin in block bb is not certified quiet (saturated towards
+        // its current value).  zz = +-z (sign of x_i): quiet <=> zz > B0 + B1*A (see B0, B1).
+        auto scan_one = [&](uint32_t &nq, int b, int bb, bool check_valid) {
+          const float A = sAl[32 * b];
+          const float ph = phw[32 * b];
+          const bool xb = (xm >> b) & 1u;
+          const float Asg = xb ? A : -A;                   // -(A (1 - 2x_i))
+          const float v = r2 - Asg;                        // 2 r0 + A
+          const float tq = fmaf(K2, v, K3);
+          const float zz = fmaf(xb ? K1 : -K1, ph, -(Asg * tq));   // (2x_i - 1) * z
+          const bool quiet = zz > fmaf(B1, A, B0);
+          if (!quiet && (!check_valid || lane < N - 32 * b)) nq |= 1u << bb;
+        };
+        auto scan_general = [&](int bstart) -> uint32_t {
           uint32_t nq = 0;
-          auto scan_one = [&](int b, int bb, bool check_valid) {
-            const float A = sAl[32 * b];
-            const float ph = phw[32 * b];
-            const bool xb = (xm >> b) & 1u;
-            const float Asg = xb ? A : -A;                 // -(A (1 - 2x_i))
-            const float v = r2 - Asg;                      // 2 r0 + A
-            const float tq = fmaf(K2, v, K3);
-            const float zz = fmaf(xb ? K1 : -K1, ph, -(Asg * tq));   // (2x_i - 1) * z
-            const bool quiet = zz > fmaf(B1, A, B0);
-            if (!quiet && (!check_valid || lane < N - 32 * b)) nq |= 1u << bb;
-          };
-          if (bstart == 0 && 32 * (4 * g + 4) <= N) {      // hot path: four full blocks
 #pragma unroll
-            for (int bb = 0; bb < 4; ++bb) scan_one(4 * g + bb, bb, false);
-          } else {
-#pragma unroll
-            for (int bb = 0; bb < 4; ++bb)
-              if (bb >= bstart && bb < nbg) scan_one(4 * g + bb, bb, true);
-          }
-          uint32_t m = __reduce_or_sync(kFull, nq);
-          if (!m) break;                                  // common case: the group is quiet
+          for (int bb = 0; bb < 4; ++bb)
+            if (bb >= bstart && bb < nbg) scan_one(nq, 4 * g + bb, bb, true);
+          return __reduce_or_sync(kFull, nq);
+        };
+        // Process the non-quiet blocks of group g in order (exactly); after a flip the later
+        // blocks' speculation is stale, so they are rescanned.
+        auto handle_group = [&](uint32_t m) {
           active = true;
-          bool flipped = false;
-          while (m) {                                     // active blocks, in order
-            const int bb = __ffs(m) - 1;
-            m &= m - 1u;
-            if (process_block(4 * g + bb, bb)) {          // a flip invalidates the later speculation
-              flipped = true;
-              bstart = bb + 1;
-              break;
+          for (;;) {
+            int bstart = 4;
+            while (m) {
+              const int bb = __ffs(m) - 1;
+              m &= m - 1u;
+              if (process_block(4 * g + bb, bb)) { bstart = bb + 1; break; }
             }
+            if (bstart >= nbg) return;
+            m = scan_general(bstart);
+            if (!m) return;
           }
-          if (!flipped || bstart >= nbg) break;
+        };
+
+        const int NGF = N >> 7;                           // groups of four full blocks
+        for (g = 0; g < NGF; ++g) {                       // hot path
+          have_u = false;
+          nbg = 4;
+          uint32_t nq = 0;
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) scan_one(nq, 4 * g + bb, bb, false);
+          const uint32_t m = __reduce_or_sync(kFull, nq);
+          if (m) handle_group(m);
         }
-      }
+        for (; 4 * g < NB; ++g) {                         // the ragged tail group
+          have_u = false;
+          nbg = min(4, NB - 4 * g);
+          const uint32_t m = scan_general(0);
+          if (m) handle_group(m);
+        }
       cnt_add(ws, kCntSweeps, 1);
       // Frozen anneal: a sweep in which every spin was certified
       // saturated towards its current value changed nothing; fields stay constant and beta only
