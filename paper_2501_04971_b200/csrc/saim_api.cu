@@ -23,9 +23,9 @@ namespace saim {
 int qkp_npl_bucket(int npl);
 cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *max_wpc);
 cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st);
-int mkp_plan(int n, int M, int n_slack_max, int *lanes, int *smem_bytes, int *max_wpc);
-cudaError_t mkp_launch(const RunArgs &a, int n_inst, int lanes, int wpc, int smem_bytes, cudaStream_t st);
-void mkp_blob_layout(int n, int M, int n_slack_max, uint32_t *a_off, uint32_t *c_off, uint32_t *x_off, uint32_t *bytes);
+int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
+             int *max_wpc);
+cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
 int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 }  // namespace saim
 
@@ -52,7 +52,9 @@ struct saim_ctx {
   int n_inst = 0, n = 0, M = 0;
   int kernel = 0;       // 1 = QKP, 2 = MKP
   int npl = 0, qb = 0;  // QKP
-  int lanes = 32;       // MKP lanes per replica
+  int lanes = 32;       // lanes per replica (QKP: 32; MKP: 1, lockstep)
+  int mm = 0;           // MKP padded constraint count
+  uint32_t per_warp = 0;
   int N_max = 0, n_slack_max = 0;
   int smem_bytes = 0, max_wpc = 32, sm_count = 148;
   uint32_t blob_bytes = 0, a_off = 0, c_off = 0, x_off = 0;
@@ -170,6 +172,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
         for (int j = 0; j < n; ++j) amax = std::max(amax, (long long)A[(size_t)k * n + j]);
       }
       h.v_bound = 2.0 * (double)rmax + (double)amax;
+      h.r_bound = (double)rmax;
     }
     ctx->N_max = std::max(ctx->N_max, h.N);
     ctx->n_slack_max = std::max(ctx->n_slack_max, n_slack);
@@ -244,36 +247,46 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "configure QKP kernel"); }
     ctx->lanes = 32;
   } else if (!prob->Q) {
-    // ---------------- MKP kernel layout ----------------
+    // ---------------- MKP kernel layout (saim_layout.h MkpLayout) ----------------
     ctx->kernel = 2;
-    int lanes = 0, smem = 0, mw = 0;
-    if (mkp_plan(n, M, ctx->n_slack_max, &lanes, &smem, &mw) != 0 || smem + 64 > smem_optin) {
+    ctx->lanes = 1;
+    if (mkp_plan(n, M, ctx->N_max, smem_optin, &ctx->mm, &ctx->blob_bytes, &ctx->per_warp, &ctx->max_wpc) != 0) {
       delete ctx;
-      return fail(SAIM_ESMEM, "MKP instance (n=%d, M=%d) does not fit shared memory", n, M);
+      return fail(SAIM_ESMEM, "MKP instance (n=%d, M=%d, N=%d) does not fit shared memory", n, M, ctx->N_max);
     }
-    for (int s = 0; s < S; ++s)
-      for (int k = 0; k < M; ++k)
-        for (int j = 0; j < n; ++j)
-          if (prob->A[((size_t)s * M + k) * n + j] > 32767) {
-            delete ctx;
-            return fail(SAIM_ERANGE, "MKP weights must be <= 32767 (int16 columns)");
-          }
-    ctx->lanes = lanes; ctx->smem_bytes = smem; ctx->max_wpc = mw;
-    mkp_blob_layout(n, M, ctx->n_slack_max, &ctx->a_off, &ctx->c_off, &ctx->x_off, &ctx->blob_bytes);
+    const int MM = ctx->mm;
+    const MkpLayout L = mkp_layout(n, MM);
+    ctx->smem_bytes = (int)(L.bytes + ctx->per_warp);
     blob.assign((size_t)S * ctx->blob_bytes, 0);
-    const int n_pad = (n + 1) & ~1;
     for (int s = 0; s < S; ++s) {
       unsigned char *B = blob.data() + (size_t)s * ctx->blob_bytes;
-      int16_t *Acol = reinterpret_cast<int16_t *>(B + ctx->a_off);      // [n_pad][M]
-      for (int j = 0; j < n; ++j)
-        for (int k = 0; k < M; ++k) Acol[(size_t)j * M + k] = (int16_t)prob->A[((size_t)s * M + k) * n + j];
-      int32_t *cc = reinterpret_cast<int32_t *>(B + ctx->c_off);
-      for (int i = 0; i < n; ++i) cc[i] = prob->c[(size_t)s * n + i];
-      (void)n_pad;
-      uint16_t *sl = reinterpret_cast<uint16_t *>(B + ctx->x_off);       // (row << 8) | shift
-      int idx = 0;
-      for (int k = 0; k < M; ++k)
-        for (int bit = 0; bit < ctx->q[s][k]; ++bit) sl[idx++] = (uint16_t)((k << 8) | bit);
+      const InstHdr &h = ctx->hdr[s];
+      float *acol = reinterpret_cast<float *>(B + L.acol);
+      float *ic = reinterpret_cast<float *>(B + L.iconst);
+      int32_t *cc = reinterpret_cast<int32_t *>(B + L.cint);
+      int64_t *brow = reinterpret_cast<int64_t *>(B + L.brow);
+      int32_t *qrow = reinterpret_cast<int32_t *>(B + L.qrow);
+      for (int i = 0; i < n; ++i) {
+        double a2 = 0.0, a1 = 0.0;
+        for (int k = 0; k < M; ++k) {
+          const double v = (double)prob->A[((size_t)s * M + k) * n + i];
+          acol[(size_t)i * MM + k] = (float)v;
+          a2 += v * v;
+          a1 += v;
+        }
+        const int32_t ci = prob->c[(size_t)s * n + i];
+        const float cphi = (float)(-h.c_o * (double)ci), cpa = (float)(h.c_p * a2);
+        ic[4 * i + 0] = cphi;
+        ic[4 * i + 1] = cpa;
+        ic[4 * i + 2] = (float)a1;
+        // E0_i = 2 (MM+6) 2^-24 (|c_o c_i| + c_p a_i), DESIGN.md 6.2 (factor 2: margin)
+        ic[4 * i + 3] = (float)(2.0 * (MM + 6) * 0x1p-24 * (fabs((double)cphi) + (double)cpa));
+        cc[i] = ci;
+      }
+      for (int k = 0; k < M; ++k) {
+        brow[k] = prob->b[(size_t)s * M + k];
+        qrow[k] = ctx->q[s][k];
+      }
     }
   } else {
     delete ctx;
@@ -328,11 +341,10 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
     e = qkp_launch(ctx->npl, ctx->qb, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
   } else {
-    const int rpw = 32 / ctx->lanes;                     // replicas per warp
-    const long long warps = ((long long)R * ctx->n_inst + rpw - 1) / rpw;
+    const long long warps = (long long)((R + 31) / 32) * ctx->n_inst;   // 32 replicas per warp (lockstep)
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
-    e = mkp_launch(a, ctx->n_inst, ctx->lanes, wpc, ctx->smem_bytes, st);
+    e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SAIM_OK;

@@ -38,7 +38,35 @@ struct InstHdr {
   int32_t pad;
   double phi_bound;   // max_i |c_i| + sum_j |Q_ij|  >= |phi_i| for every state (host-proven)
   double v_bound;     // 2 max|r| + max A_ext      >= |2 r0 + A_i| for every state
+  double r_bound;     // max|r_k| over every state and row (host-proven)
 };
+
+inline __host__ __device__ uint32_t align16u(uint32_t v) { return (v + 15u) & ~15u; }
+
+// MKP blob (per instance), MM = padded constraint count (4, 8, 16 or 32):
+//   acol   float [n][MM]   item columns A[.][i], zero-padded rows m >= M
+//   iconst float4[n]       (c_o*phi_i = -c_o c_i, c_p a_i with a_i = sum_m A_mi^2, |A_i|_1, E0_i)
+//   cint   int32 [n]       c_i (exact objective for the readout)
+//   brow   int64 [MM]      b_m
+//   qrow   int32 [MM]      slack bit count q_m (0 for padded rows)
+struct MkpLayout {
+  uint32_t acol, iconst, cint, brow, qrow, bytes;
+};
+inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
+  MkpLayout L;
+  uint32_t o = 0;
+  L.acol = o;   o += align16u((uint32_t)n * MM * 4u);
+  L.iconst = o; o += (uint32_t)n * 16u;
+  L.cint = o;   o += align16u((uint32_t)n * 4u);
+  L.brow = o;   o += (uint32_t)MM * 8u;
+  L.qrow = o;   o += align16u((uint32_t)MM * 4u);
+  L.bytes = o;
+  return L;
+}
+// Per-warp MKP shared memory: x bits [WN][32 lanes], Philox word stash [96][32], Lambda [MM][32] int64.
+inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM) {
+  return align16u((uint32_t)WN * 128u) + 96u * 128u + (uint32_t)MM * 256u;
+}
 
 struct RunArgs {
   const unsigned char *blob;  // [n_inst][blob_bytes]

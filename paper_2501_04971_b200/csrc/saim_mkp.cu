@@ -1,11 +1,372 @@
-// saim_mkp.cu -- fused SAIM kernel for linear objectives with M <= 32 constraints (MKP).
-// (placeholder: planned in DESIGN.md; saim_create rejects MKP until it lands)
-#include <cuda_runtime.h>
+// saim_mkp.cu -- fused SAIM kernel for linear objectives with 2 <= M <= 32 constraints (MKP,
+// PAPER.md:321-326; BASELINE.json configs 3-4).  sm_100a.
+//
+// Mapping: one LANE = one replica, one warp = 32 replicas of the same instance
+// marching through the spins in lockstep.  Every lane makes every decision of its own chain in
+// the exact sequential order of Algorithm 1 / Eq. 9-10 -- there is no speculation, so the ~25%
+// flip rate of MKP anneals costs nothing extra -- while the instance data a step needs (the item
+// column A_{.i}, its constants) is the same for all lanes: one shared-memory broadcast.
+//
+// Field of spin i (R1), with r = A_ext x - b, Lambda the Lagrange accumulator (R10):
+//   item i:   F_i = -c_o c_i - c_p a_i (1 - 2x_i) - 2 c_p (A_{.i} . r) - c_l (A_{.i} . Lambda)
+//   slack bit q of row m (A = 2^q):  F = -A (2 c_p r_m + c_l Lambda_m) - c_p A^2 (1 - 2x)
+// r is kept as exact integers in fp32 registers (|r| < 2^21, host-proven); the dot products are
+// fp32 with a rigorous error bound; c_l Lambda_m is rounded once per iteration.
+// Decisions are certified exactly as in the QKP kernel: saturated test, fp32 logit band, fp64
+// slow path (counted when even that is not certain).
 #include <cstdint>
-#include "saim_layout.h"
+#include <cstdio>
+
+#include "saim_dev.cuh"
 
 namespace saim {
-int mkp_plan(int, int, int, int *, int *, int *) { return -1; }
-void mkp_blob_layout(int, int, int, uint32_t *a, uint32_t *c, uint32_t *x, uint32_t *bytes) { *a = *c = *x = *bytes = 0; }
-cudaError_t mkp_launch(const RunArgs &, int, int, int, int, cudaStream_t) { return cudaErrorNotSupported; }
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// fp64 tail of the slow path: z and its magnitude sum S are accurate to ~2^-50 S; returns
+// (x | uncertified << 1).
+__device__ __noinline__ int certify_fp64(double zz, double S, uint32_t w) {
+  const double d = zz - logit_f64(w);
+  return (d > 0.0 ? 1 : 0) | (fabs(d) <= (S + 1.0 + fabs(zz)) * 0x1p-46 ? 2 : 0);
+}
+
+template <int MM>
+struct MkpCfg {
+  static constexpr int kThreads = MM <= 16 ? 512 : 256;
+};
+
+}  // namespace
+
+template <int MM>
+__global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const RunArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t mbar;
+
+  const int s = blockIdx.y;
+  bulk_stage(smem, a.blob + (size_t)s * a.blob_bytes, a.blob_bytes, &mbar);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ridx = (blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane;
+  const int wfirst = (blockIdx.x * (blockDim.x >> 5) + warp) * 32;
+  if (wfirst >= a.R) return;                         // whole warp beyond R
+  const bool live = ridx < a.R;                        // lanes beyond R compute but never write
+  const int rho = a.rep0 + (live ? ridx : a.R - 1);
+  const InstHdr *Hp = a.hdr + s;
+  const int n = a.n, M = a.M;
+  const int N = Hp->N;
+  const MkpLayout L = mkp_layout(n, MM);
+  const float *sAcol = reinterpret_cast<const float *>(smem + L.acol);
+  const float4 *sIc = reinterpret_cast<const float4 *>(smem + L.iconst);
+  const int32_t *sC = reinterpret_cast<const int32_t *>(smem + L.cint);
+  const long long *sB = reinterpret_cast<const long long *>(smem + L.brow);
+  const int32_t *sQ = reinterpret_cast<const int32_t *>(smem + L.qrow);
+  unsigned char *wbase = smem + a.blob_bytes + warp * mkp_warp_bytes(a.WN, MM);
+  uint32_t *xw = reinterpret_cast<uint32_t *>(wbase) + lane;                            // word w: xw[32 w]
+  uint32_t *stash = reinterpret_cast<uint32_t *>(wbase + align16u(a.WN * 128u)) + lane;  // [3 slot + j]
+  long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + 96u * 128u) + lane;  // [m]
+
+  const double c_o = Hp->c_o, c_p = Hp->c_p, c_l = Hp->c_l;
+  const float twocp = (float)(2.0 * c_p), cpf = (float)c_p;
+  const float rbound = (float)Hp->r_bound;
+
+  float r[MM], cL[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    r[m] = m < M ? (float)(-sB[m]) : 0.0f;             // x = 0: r = -b
+    cL[m] = 0.0f;
+    Lam[32 * m] = 0;
+  }
+  for (int w = 0; w < a.WN; ++w) xw[32 * w] = 0u;
+  long long best_f = LLONG_MAX;
+  int best_k = -1, nfeas = 0;
+  uint32_t c_flips = 0, c_unif = 0, c_fp64 = 0, c_unc = 0, c_philox = 0;
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
+  const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
+  const int Wn = (n + 31) >> 5;
+
+  for (int k = 0; k < a.K; ++k) {
+    // ---- per-iteration constants: c_l Lambda_m (rounded once), error-bound slope E1 ----
+    float cLmax = 0.0f;
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      cL[m] = (float)(c_l * (double)Lam[32 * m]);
+      cLmax = fmaxf(cLmax, fabsf(cL[m]));
+    }
+    // |z_f32 - z| <= beta (E1 |A_i|_1 + E0_i) + 2^-23 |z|, E = (MM+6) 2^-24 (...);
+    // the factor 2 below is a safety margin.
+    const float E1 = (float)((MM + 6) * 0x1p-24 * (2.0 * c_p * (double)rbound + (double)cLmax)) * 2.0f;
+
+    for (int t = 0; t < a.T; ++t) {
+      const bool bz = (a.T >= 2) && (t == 0);          // beta_0 = 0: x_i = [u < 1/2]
+      const double beta = (a.T >= 2) ? bstep * (double)t : a.beta_max;
+      const float bf = (float)beta;
+      uint32_t xcur = 0;
+
+      // Uniform word of spin i (R2): the Philox call of counter (32 floor(i/128) + i%32, t, k,
+      // s<<20|rho) yields the words of spins i, i+32, i+64, i+96; three are stashed per lane.
+      auto uword = [&](int i) -> uint32_t {
+        const int j = i & 127;
+        if (j < 32) {
+          const uint4 w4 = philox_group(key, i >> 7, j, t, k, srho);
+          ++c_philox;
+          stash[32 * (3 * j + 0)] = w4.y;
+          stash[32 * (3 * j + 1)] = w4.z;
+          stash[32 * (3 * j + 2)] = w4.w;
+          return w4.x;
+        }
+        return stash[32 * (3 * (j & 31) + (j >> 5) - 1)];
+      };
+      // Certified decision [u < sigma(z)] (R18, R19) given z, its error bound e and the word w;
+      // slow(): fp64 re-evaluation returning (x | uncertified << 1).
+      auto decide = [&](float z, float e, uint32_t w, auto slow) -> int {
+        if (bz) return (w >> 31) == 0u;                 // u < 1/2
+        if (fabsf(z) - e > kSatThr) return z > 0.0f;
+        ++c_unif;
+        const float l = logit_f32(w);
+        const float d = z - l;
+        if (fabsf(d) > (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f) return d > 0.0f;
+        ++c_fp64;
+        const int rs = slow();
+        if (rs & 2) ++c_unc;
+        return rs & 1;
+      };
+
+      // ---- items i = 0..n-1 ----
+      for (int i = 0; i < n; ++i) {
+        if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
+        const uint32_t w = uword(i);
+        const int xb = (xcur >> (i & 31)) & 1u;
+        const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
+        float dr0 = 0.f, dr1 = 0.f, dl0 = 0.f, dl1 = 0.f;
+#pragma unroll
+        for (int m4 = 0; m4 < MM / 4; ++m4) {
+          const float4 av = Ac[m4];
+          dr0 = fmaf(av.x, r[4 * m4 + 0], dr0); dr1 = fmaf(av.y, r[4 * m4 + 1], dr1);
+          dr0 = fmaf(av.z, r[4 * m4 + 2], dr0); dr1 = fmaf(av.w, r[4 * m4 + 3], dr1);
+          dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1);
+          dl0 = fmaf(av.z, cL[4 * m4 + 2], dl0); dl1 = fmaf(av.w, cL[4 * m4 + 3], dl1);
+        }
+        const float4 ic = sIc[i];                        // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
+        const float sg = xb ? -1.0f : 1.0f;              // 1 - 2 x_i
+        const float F = fmaf(-twocp, dr0 + dr1, fmaf(-ic.y, sg, ic.x)) - (dl0 + dl1);
+        const float z = bf * F;
+        const float e = bf * fmaf(E1, ic.z, ic.w) + fabsf(z) * 0x1p-22f;
+        const int nx = decide(z, e, w, [&]() -> int {
+          double dr = 0.0, dl = 0.0, a2 = 0.0;
+#pragma unroll
+          for (int m = 0; m < MM; ++m) {
+            const double Am = (double)sAcol[i * MM + m];
+            dr += Am * (double)r[m];
+            dl += Am * (double)Lam[32 * m];
+            a2 += Am * Am;
+          }
+          const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * dr, t4 = c_l * dl;
+          const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
+          return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), w);
+        });
+        const float dl = (float)(nx - xb);                  // delta in {-1, 0, +1}
+        if (__any_sync(kFull, nx != xb)) {
+#pragma unroll
+          for (int m4 = 0; m4 < MM / 4; ++m4) {
+            const float4 av = Ac[m4];
+            r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
+            r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
+            r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
+            r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
+          }
+        }
+        if (nx != xb) { xcur ^= 1u << (i & 31); ++c_flips; }
+        if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
+      }
+      // ---- slack bits: row m, bit q, spin i = n + sum_{m'<m} q_m' + q (R4) ----
+      int i = n;
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const int qm = (m < M) ? sQ[m] : 0;
+        for (int q = 0; q < qm; ++q, ++i) {
+          if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
+          const uint32_t w = uword(i);
+          const int xb = (xcur >> (i & 31)) & 1u;
+          const float A = (float)(1u << q);
+          const float sg = xb ? -1.0f : 1.0f;
+          const float inner = fmaf(twocp, r[m], cL[m]);
+          const float F = -(A * inner) - (cpf * A) * A * sg;
+          const float z = bf * F;
+          const float e = bf * 8.0f * 0x1p-24f * fmaf(A, fabsf(twocp * r[m]) + fabsf(cL[m]), cpf * A * A) +
+                          fabsf(z) * 0x1p-22f;
+          const int nx = decide(z, e, w, [&]() -> int {
+            const double Ad = (double)A;
+            const double t1 = Ad * 2.0 * c_p * (double)r[m], t2 = Ad * c_l * (double)Lam[32 * m];
+            const double t3 = c_p * Ad * Ad;
+            const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
+            return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
+          });
+          if (nx != xb) {
+            r[m] = fmaf((float)(nx - xb), A, r[m]);
+            xcur ^= 1u << (i & 31);
+            ++c_flips;
+          }
+          if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
+        }
+      }
+    }
+
+    // ---- readout of x_k: f, feasibility, trace, best, Lagrange step ----
+    long long f = 0;
+    for (int w = 0; w < Wn; ++w) {
+      uint32_t bits = xw[32 * w];
+      if (32 * w + 32 > n) bits &= (1u << (n - 32 * w)) - 1u;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        f += sC[32 * w + b];
+      }
+    }
+    // feasible <=> A x_items <= b  <=>  r_m <= (slack value of row m) for every row (R12)
+    bool feas = true;
+    {
+      int i0 = n;
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const int qm = (m < M) ? sQ[m] : 0;
+        if (qm > 0) {
+          long long sv = 0;
+          for (int q = 0; q < qm; ++q) {
+            const int i = i0 + q;
+            sv += (long long)((xw[32 * (i >> 5)] >> (i & 31)) & 1u) << q;
+          }
+          if ((long long)r[m] > sv) feas = false;
+        }
+        i0 += qm;
+      }
+    }
+    const size_t row = ((size_t)s * a.R + ridx) * a.K + k;
+    if (live) {
+      if (a.out.tr_f) a.out.tr_f[row] = f;
+      if (a.out.tr_feas) a.out.tr_feas[row] = (uint8_t)feas;
+      for (int m = 0; m < M; ++m) {
+        if (a.out.tr_lam) a.out.tr_lam[row * M + m] = Lam[32 * m];
+      }
+      if (a.out.tr_x)
+        for (int w = 0; w < a.WN; ++w) a.out.tr_x[row * a.WN + w] = xw[32 * w];
+    }
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      if (m < M) {
+        const long long rl = (long long)r[m];
+        if (live && a.out.tr_r) a.out.tr_r[row * M + m] = rl;
+        Lam[32 * m] += rl;                                 // lambda_{k+1} = lambda_k + eta g(x_k) (R10)
+      }
+    }
+    if (feas) {
+      ++nfeas;
+      if (f < best_f) {
+        best_f = f;
+        best_k = k;
+        if (live) {
+          const size_t ri = (size_t)s * a.R + ridx;
+          for (int w = 0; w < Wn; ++w) {
+            uint32_t bits = xw[32 * w];
+            if (32 * w + 32 > n) bits &= (1u << (n - 32 * w)) - 1u;
+            a.out.best_x[ri * a.Wn + w] = bits;
+          }
+        }
+      }
+    }
+  }
+
+  // ---- outputs ----
+  const size_t ri = (size_t)s * a.R + ridx;
+  if (live) {
+    a.out.best_f[ri] = best_f;
+    a.out.best_k[ri] = best_k;
+    a.out.n_feasible[ri] = nfeas;
+    if (best_k < 0)
+      for (int w = 0; w < Wn; ++w) a.out.best_x[ri * a.Wn + w] = 0u;
+    if (a.out.final_x)
+      for (int w = 0; w < a.WN; ++w) a.out.final_x[ri * a.WN + w] = xw[32 * w];
+    if (a.out.final_lam)
+      for (int m = 0; m < M; ++m) a.out.final_lam[ri * M + m] = Lam[32 * m];
+  }
+  // per-instance best (f << 20 | rho): warp min, one atomic
+  long long key_best = (live && best_k >= 0) ? ((best_f << 20) | (long long)rho) : LLONG_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long other = __shfl_xor_sync(kFull, key_best, o);
+    key_best = other < key_best ? other : key_best;
+  }
+  if (lane == 0 && key_best != LLONG_MAX && a.out.inst_best)
+    atomicMin(reinterpret_cast<long long *>(a.out.inst_best) + s, key_best);
+  if (a.out.counters) {
+    const unsigned long long nl = live ? 1ull : 0ull;
+    const unsigned long long fl = warp_sum_u64(nl * c_flips), un = warp_sum_u64(nl * c_unif);
+    const unsigned long long fp = warp_sum_u64(nl * c_fp64), uc = warp_sum_u64(nl * c_unc);
+    const unsigned long long ph = warp_sum_u64(nl * c_philox), nf = warp_sum_u64(nl * (unsigned long long)nfeas);
+    const unsigned long long lv = warp_sum_u64(nl);
+    if (lane == 0) {
+      unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
+      atomicAdd(c + SAIM_CNT_DECISIONS, lv * (unsigned long long)a.K * a.T * N);
+      atomicAdd(c + SAIM_CNT_FLIPS, fl);
+      atomicAdd(c + SAIM_CNT_SWEEPS, lv * (unsigned long long)a.K * a.T);
+      atomicAdd(c + SAIM_CNT_UNIFORMS, un);
+      atomicAdd(c + SAIM_CNT_FP64, fp);
+      atomicAdd(c + SAIM_CNT_UNCERTIFIED, uc);
+      atomicAdd(c + SAIM_CNT_FEASIBLE, nf);
+      atomicAdd(c + SAIM_CNT_PHILOX, ph);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+typedef void (*mkp_kernel_t)(const RunArgs);
+
+static int mm_for(int M) { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : -1))); }
+
+static mkp_kernel_t mkp_kernel_for(int MM) {
+  switch (MM) {
+    case 4: return saim_mkp_kernel<4>;
+    case 8: return saim_mkp_kernel<8>;
+    case 16: return saim_mkp_kernel<16>;
+    case 32: return saim_mkp_kernel<32>;
+    default: return nullptr;
+  }
+}
+
+// Plan the MKP launch: padded constraint count MM, blob layout, per-warp bytes and the maximum
+// warps per CTA allowed by threads/registers and shared memory.  Returns 0 or -1 (does not fit).
+int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
+             int *max_wpc) {
+  const int MM = mm_for(M);
+  if (MM < 0) return -1;
+  mkp_kernel_t k = mkp_kernel_for(MM);
+  cudaFuncAttributes attr;
+  if (cudaFuncGetAttributes(&attr, k) != cudaSuccess) return -1;
+  const MkpLayout L = mkp_layout(n, MM);
+  const int WN = (N_max + 31) / 32;
+  const uint32_t pw = mkp_warp_bytes(WN, MM);
+  int wpc = attr.maxThreadsPerBlock / 32;
+  const long long by_smem = ((long long)smem_optin - L.bytes - attr.sharedSizeBytes - 64) / pw;
+  if (by_smem < wpc) wpc = (int)by_smem;
+  if (wpc < 1) return -1;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(L.bytes + wpc * pw)) != cudaSuccess)
+    return -1;
+  *MM_out = MM;
+  *blob_bytes = L.bytes;
+  *per_warp = pw;
+  *max_wpc = wpc;
+  return 0;
+}
+
+cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st) {
+  mkp_kernel_t k = mkp_kernel_for(MM);
+  if (!k) return cudaErrorInvalidValue;
+  const int warps_per_inst = (a.R + 31) / 32;
+  dim3 grid((warps_per_inst + wpc - 1) / wpc, n_inst);
+  k<<<grid, wpc * 32, a.blob_bytes + wpc * per_warp, st>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace saim

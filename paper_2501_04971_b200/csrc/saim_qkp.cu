@@ -32,10 +32,6 @@ namespace saim {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
-// |logit_f32(u) - logit(u)| <= kLogitAbs + kLogitRel * |logit(u)| for every representable u
-// (checked exhaustively over all 2^23 uniforms by tests/test_gpu_parity.py).
-constexpr float kLogitAbs = 0x1p-17f;
-constexpr float kLogitRel = 0x1p-19f;
 // fp32 field: |z_f32 - z| <= 2^-20 * S with S = |K1 phi| + |A|(|K2 v| + |K3|).  The true bound
 // is ~3 * 2^-24 (three roundings plus fp32-rounded constants): a 5x margin.  The saturation test
 // |z| - 2^-20 S > ln(2^24-1) is evaluated as fl(z * (+-2^20) - S) > 2^20 * kSatThr (one FFMA with
@@ -47,17 +43,6 @@ constexpr int kQkpMaxThreads = 896;
 
 __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
   return i == 0 ? u.x : (i == 1 ? u.y : (i == 2 ? u.z : u.w));
-}
-
-__device__ __forceinline__ float lg2_approx(float x) {   // MUFU.LG2; inputs here are normal
-  float y;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ float logit_f32(uint32_t w) {
-  const float u = uniform_f32(w);
-  return (lg2_approx(u) - lg2_approx(1.0f - u)) * 0.693147180559945309f;
 }
 
 // Lazily drawn uniforms: kept out of line so the compiler cannot hoist the 10-round Philox into

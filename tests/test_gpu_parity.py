@@ -214,3 +214,41 @@ def test_freeze_exit_is_exact(P, cfg_idx):
         assert on["counters"][k] == off["counters"][k], k
     assert off["counters"]["sweeps"] == R * K * cfg.T * len(cfg.instances)
     assert on["counters"]["sweeps"] <= off["counters"]["sweeps"]
+
+
+# ---------------------------------------------------------------------------------------------
+# MKP kernel (linear objective, M >= 2; BASELINE configs 3-4)
+
+def _mkp(n, m, t, seed):
+    return si.mkp(n, m, t, [88, n, m, seed])
+
+
+@pytest.mark.parametrize("n,m", [(7, 2), (30, 3), (33, 5), (64, 8), (40, 9), (20, 16), (25, 30)])
+def test_mkp_parity_small(P, n, m):
+    """Small MKP instances across the constraint-count buckets (MM = 4, 8, 16, 32) with ragged N."""
+    p = _mkp(n, m, 0.5, 1)
+    g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=40, K=4, T=30)
+    assert g["info"]["kernel"] == 2
+
+
+def test_mkp_parity_tiny_capacities(P):
+    p = _mkp(12, 3, 0.1, 2)
+    p.b[:] = [1, 2, 3]
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=5, T=25)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=3, T=1)      # fixed beta
+
+
+def test_mkp_parity_config3_sampled(P):
+    """Config 3 (three tightness variants in one launch) at full size; sampled replicas."""
+    cfg = si.config_instances(3)
+    run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
+             reps=[0, 2047])
+
+
+def test_mkp_parity_config4_sampled(P):
+    """Config 4 shape (64 instances x 256 replicas, n=500, M=30) with K reduced to 4 so the
+    oracle can replay sampled replicas; the launch configuration is the full one."""
+    cfg = si.config_instances(4)
+    g = run_both(P, cfg.instances[:8], cfg.P[:8], cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=4, T=cfg.T,
+                 reps=[0, 255])
+    assert g["info"]["kernel"] == 2
