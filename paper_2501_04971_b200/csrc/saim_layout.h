@@ -63,9 +63,10 @@ inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
   L.bytes = o;
   return L;
 }
-// Per-warp MKP shared memory: x bits [WN][32 lanes], Philox word stash [96][32], Lambda [MM][32] int64.
+// Per-warp MKP shared memory: x bits [WN][32 lanes], logits of the current 128-spin group
+// [128][32] floats, Lambda [MM][32] int64.
 inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM) {
-  return align16u((uint32_t)WN * 128u) + 96u * 128u + (uint32_t)MM * 256u;
+  return align16u((uint32_t)WN * 128u) + 128u * 128u + (uint32_t)MM * 256u;
 }
 
 struct RunArgs {

@@ -32,6 +32,19 @@ __device__ __noinline__ int certify_fp64(double zz, double S, uint32_t w) {
   return (d > 0.0 ? 1 : 0) | (fabs(d) <= (S + 1.0 + fabs(zz)) * 0x1p-46 ? 2 : 0);
 }
 
+// Uniform word of spin i (R2) recomputed for the slow path.
+__device__ __noinline__ uint32_t word_of(uint2 key, int i, int t, int k, uint32_t srho) {
+  const uint4 w4 = philox_group(key, i >> 7, i & 31, t, k, srho);
+  const int j = (i >> 5) & 3;
+  return j == 0 ? w4.x : (j == 1 ? w4.y : (j == 2 ? w4.z : w4.w));
+}
+
+// logit(u) in fp32 with its sign made exact (sign(logit u) = sign(u - 1/2) <=> w >= 2^31).
+__device__ __forceinline__ float logit_signed(uint32_t w) {
+  const float l = fabsf(logit_f32(w));
+  return (w >> 31) ? l : -l;
+}
+
 template <int MM>
 struct MkpCfg {
   static constexpr int kThreads = MM <= 16 ? 512 : 256;
@@ -64,8 +77,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
   const int32_t *sQ = reinterpret_cast<const int32_t *>(smem + L.qrow);
   unsigned char *wbase = smem + a.blob_bytes + warp * mkp_warp_bytes(a.WN, MM);
   uint32_t *xw = reinterpret_cast<uint32_t *>(wbase) + lane;                            // word w: xw[32 w]
-  uint32_t *stash = reinterpret_cast<uint32_t *>(wbase + align16u(a.WN * 128u)) + lane;  // [3 slot + j]
-  long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + 96u * 128u) + lane;  // [m]
+  float *lt = reinterpret_cast<float *>(wbase + align16u(a.WN * 128u)) + lane;           // logit of spin 128g+j: lt[32 j]
+  long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + 128u * 128u) + lane;  // [m]
 
   const double c_o = Hp->c_o, c_p = Hp->c_p, c_l = Hp->c_l;
   const float twocp = (float)(2.0 * c_p), cpf = (float)c_p;
@@ -105,27 +118,27 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       const float bf = (float)beta;
       uint32_t xcur = 0;
 
-      // Uniform word of spin i (R2): the Philox call of counter (32 floor(i/128) + i%32, t, k,
-      // s<<20|rho) yields the words of spins i, i+32, i+64, i+96; three are stashed per lane.
-      auto uword = [&](int i) -> uint32_t {
-        const int j = i & 127;
-        if (j < 32) {
-          const uint4 w4 = philox_group(key, i >> 7, j, t, k, srho);
-          ++c_philox;
-          stash[32 * (3 * j + 0)] = w4.y;
-          stash[32 * (3 * j + 1)] = w4.z;
-          stash[32 * (3 * j + 2)] = w4.w;
-          return w4.x;
+      // Logits of the uniforms of spins 128g .. 128g+127 (R2: the Philox call of counter
+      // (32g + j, t, k, s<<20|rho) yields the words of spins 128g + 32w + j, w = 0..3).  They do
+      // not depend on the state, so they are drawn in one ILP-friendly burst per group, off the
+      // sequential dependency chain of the decisions.
+      auto fill_group = [&](int g) {
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const uint4 w4 = philox_group(key, g, j, t, k, srho);
+          lt[32 * (j + 0)] = logit_signed(w4.x);
+          lt[32 * (j + 32)] = logit_signed(w4.y);
+          lt[32 * (j + 64)] = logit_signed(w4.z);
+          lt[32 * (j + 96)] = logit_signed(w4.w);
         }
-        return stash[32 * (3 * (j & 31) + (j >> 5) - 1)];
+        c_philox += 32;
       };
-      // Certified decision [u < sigma(z)] (R18, R19) given z, its error bound e and the word w;
-      // slow(): fp64 re-evaluation returning (x | uncertified << 1).
-      auto decide = [&](float z, float e, uint32_t w, auto slow) -> int {
-        if (bz) return (w >> 31) == 0u;                 // u < 1/2
+      // Certified decision [u < sigma(z)] (R18, R19) from z, its error bound e and l = logit(u)
+      // (exact sign); slow(): fp64 re-evaluation returning (x | uncertified << 1).
+      auto decide = [&](float z, float e, float l, auto slow) -> int {
+        if (bz) return (int)(__float_as_uint(l) >> 31);  // beta_0 = 0: u < 1/2 (sign bit, -0 included)
         if (fabsf(z) - e > kSatThr) return z > 0.0f;
         ++c_unif;
-        const float l = logit_f32(w);
         const float d = z - l;
         if (fabsf(d) > (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f) return d > 0.0f;
         ++c_fp64;
@@ -137,7 +150,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // ---- items i = 0..n-1 ----
       for (int i = 0; i < n; ++i) {
         if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
-        const uint32_t w = uword(i);
+        if ((i & 127) == 0) fill_group(i >> 7);
+        const float l = lt[32 * (i & 127)];
         const int xb = (xcur >> (i & 31)) & 1u;
         const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
         float dr0 = 0.f, dr1 = 0.f, dl0 = 0.f, dl1 = 0.f;
@@ -154,7 +168,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         const float F = fmaf(-twocp, dr0 + dr1, fmaf(-ic.y, sg, ic.x)) - (dl0 + dl1);
         const float z = bf * F;
         const float e = bf * fmaf(E1, ic.z, ic.w) + fabsf(z) * 0x1p-22f;
-        const int nx = decide(z, e, w, [&]() -> int {
+        const int nx = decide(z, e, l, [&]() -> int {
+          const uint32_t w = word_of(key, i, t, k, srho);
           double dr = 0.0, dl = 0.0, a2 = 0.0;
 #pragma unroll
           for (int m = 0; m < MM; ++m) {
@@ -167,16 +182,14 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
           return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), w);
         });
-        const float dl = (float)(nx - xb);                  // delta in {-1, 0, +1}
-        if (__any_sync(kFull, nx != xb)) {
+        const float dl = (float)(nx - xb);                  // delta in {-1, 0, +1}; fma(0, A, r) == r
 #pragma unroll
-          for (int m4 = 0; m4 < MM / 4; ++m4) {
-            const float4 av = Ac[m4];
-            r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
-            r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
-            r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
-            r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
-          }
+        for (int m4 = 0; m4 < MM / 4; ++m4) {
+          const float4 av = Ac[m4];
+          r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
+          r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
+          r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
+          r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
         }
         if (nx != xb) { xcur ^= 1u << (i & 31); ++c_flips; }
         if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
@@ -188,7 +201,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         const int qm = (m < M) ? sQ[m] : 0;
         for (int q = 0; q < qm; ++q, ++i) {
           if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
-          const uint32_t w = uword(i);
+          if ((i & 127) == 0) fill_group(i >> 7);
+          const float l = lt[32 * (i & 127)];
           const int xb = (xcur >> (i & 31)) & 1u;
           const float A = (float)(1u << q);
           const float sg = xb ? -1.0f : 1.0f;
@@ -197,7 +211,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           const float z = bf * F;
           const float e = bf * 8.0f * 0x1p-24f * fmaf(A, fabsf(twocp * r[m]) + fabsf(cL[m]), cpf * A * A) +
                           fabsf(z) * 0x1p-22f;
-          const int nx = decide(z, e, w, [&]() -> int {
+          const int nx = decide(z, e, l, [&]() -> int {
+            const uint32_t w = word_of(key, i, t, k, srho);
             const double Ad = (double)A;
             const double t1 = Ad * 2.0 * c_p * (double)r[m], t2 = Ad * c_l * (double)Lam[32 * m];
             const double t3 = c_p * Ad * Ad;
