@@ -188,6 +188,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2501_04971_b200 as P
+    from paper_2501_04971_b200 import dist as sdist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -200,8 +201,7 @@ def main():
 
     cfg = si.config_instances(args.config)
     Q, c, A, b = si.stack(cfg.instances)
-    R = cfg.R
-    rep0 = rank * R                     # weak scaling: each rank its own global replica range
+    rep0, R = sdist.shard_range(rank, world, cfg.R)   # weak scaling: own global replica range
     sol = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev)
     Ns = [sol.instance(s)["N"] for s in range(sol.n_inst)]
     n_items = cfg.instances[0].n
@@ -212,7 +212,7 @@ def main():
     def step(seed):
         sol.run(seed, R, cfg.K, cfg.T, rep0=rep0, out=out, stream=stream)
         if world > 1:
-            dist.all_reduce(out["inst_best"], op=dist.ReduceOp.MIN)
+            sdist.reduce_inst_best(out["inst_best"])
 
     for i in range(args.warmup):
         step(1000 + i)
@@ -291,7 +291,7 @@ def main():
         s2 = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev)
         o2 = s2.run(7 + i, R, cfg.K, cfg.T, rep0=rep0)
         if world > 1:
-            dist.all_reduce(o2["inst_best"], op=dist.ReduceOp.MIN)
+            sdist.reduce_inst_best(o2["inst_best"])
         host = {k: o2[k].cpu() for k in ["best_f", "best_x", "best_k", "n_feasible", "inst_best", "counters"]}
         e2e_times.append(time.perf_counter() - t0)
         s2.close()
