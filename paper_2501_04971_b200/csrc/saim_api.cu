@@ -205,10 +205,10 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     if (!ctx->qb) { delete ctx; return fail(SAIM_ERANGE, "|Q| entries > 32767 need wider storage"); }
     const int E = 4 / ctx->qb;
     const int QW = (ctx->npl + E - 1) / E;
-    const int NBM = ctx->npl + 2;
+    const int NBP = ((ctx->npl + 2) + 3) & ~3;            // blocks incl. padding to a 4-block group
     const uint32_t q_bytes = align16((uint32_t)n * QW * 128u);
     ctx->a_off = q_bytes;
-    ctx->c_off = ctx->a_off + align16(NBM * 32 * 4);
+    ctx->c_off = ctx->a_off + align16(NBP * 32 * 4);
     ctx->blob_bytes = ctx->c_off + align16(ctx->npl * 32 * 4);
     if ((int)ctx->blob_bytes + 64 > smem_optin) {
       delete ctx;
@@ -234,6 +234,8 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
           }
       }
       float *Aext = reinterpret_cast<float *>(B + ctx->a_off);
+      const int Ns = ctx->hdr[s].N;
+      for (int i = 0; i < NBP * 32; ++i) Aext[i] = i < Ns ? 0.0f : std::nanf("");   // NaN: no spin (scan: quiet)
       if (M == 1) {
         const int32_t *A = prob->A + (size_t)s * n;
         for (int i = 0; i < n; ++i) Aext[i] = (float)A[i];

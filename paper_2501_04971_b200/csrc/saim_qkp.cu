@@ -45,18 +45,14 @@ __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
   return i == 0 ? u.x : (i == 1 ? u.y : (i == 2 ? u.z : u.w));
 }
 
-// Lazily drawn uniforms: kept out of line so the compiler cannot hoist the 10-round Philox into
-// the common (saturated) path -- it runs only when some lane of the group needs its u.
-__device__ __noinline__ uint4 philox_group_lazy(uint2 key, int g, int lane, int t, int k, uint32_t srho) {
-  return philox_group(key, g, lane, t, k, srho);
-}
 
 // Per-warp cold state in shared memory (kept out of the register file: the hot loop runs at
 // 28 warps/SM, i.e. <= 72 registers per thread).
 struct WarpState {
-  double k1step, k2step, k3step;   // beta_t = t * bstep:  K1 = t*bstep*c_o, K2 = t*bstep*c_p, K3 = t*bstep*c_l*Lambda
+  float k1s, k2s, k3s;             // per unit t: K1 = t*bstep*c_o, K2 = t*bstep*c_p, K3 = t*bstep*c_l*Lambda
+  float e0s, e1s;                  // scan error bound per unit t: e(A) = t*(e0s + e1s*A)
+  float pad;
   double bstep;                    // beta_max / (T-1)   (or beta_max with t := 1 when T == 1)
-  double e0step, e1step;           // scan error bound per unit beta_t: e(A) = t*(e0step + e1step*A)
   long long Lam;                   // Lambda_k (Lambda_0 = 0)
   long long best_f;
   int best_k, nfeas;
@@ -78,45 +74,40 @@ __device__ __noinline__ int decide_fp64(float phib, float v, float A, int t, con
   const double Ad = (double)A, vd = (double)v, pd = (double)phib;
   const double z = fma(K1d, pd, -(Ad * fma(K2d, vd, K3d)));
   const double S = fabs(K1d * pd) + fabs(Ad) * (fabs(K2d * vd) + fabs(K3d));
-  const double u = uniform_f64(w);
-  const double l = log(u) - log1p(-u);
-  const double d = z - l;
-  const double e = (S + 1.0 + fabs(l)) * 0x1p-47;
+  const double d = z - logit_f64(w);
+  const double e = (S + 1.0 + fabs(z)) * 0x1p-47;
   return (d > 0.0 ? 1 : 0) | (fabs(d) <= e ? 2 : 0);
 }
 
-// phi_i -= delta * Q[j][i] for the lane's items i = 32m + lane (one Q row, lane-major).
-template <int NPL, int QB>
-__device__ __forceinline__ void phi_update(const uint32_t *row, float *phw, float dl) {
-  constexpr int E = 4 / QB, QW = (NPL + E - 1) / E;
-  constexpr float kQBias = (float)(1 << (8 * QB - 1));
-#pragma unroll
-  for (int w = 0; w < QW; ++w) {
-    const uint32_t word = row[32 * w];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int m = E * w + e;
-      if (m < NPL) {
-        const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
-        const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
-        phw[32 * m] = fmaf(-dl, q, phw[32 * m]);
-      }
-    }
-  }
+// Lazily drawn uniforms: the empty volatile asm is a side effect, so the compiler cannot
+// speculatively hoist the 10-round Philox into the common (saturated) path.
+__device__ __forceinline__ uint4 philox_group_lazy(uint2 key, int g, int lane, int t, int k, uint32_t srho) {
+  uint32_t x = 32u * (uint32_t)g + (uint32_t)lane;
+  asm volatile("" : "+r"(x));
+  return philox4x32_10(make_uint4(x, (uint32_t)t, (uint32_t)k, srho), key);
 }
 
 }  // namespace
 
+// Blocks of the padded spin range: NPL item blocks + up to 2 slack blocks, rounded up to a whole
+// 4-block group (spins >= N carry A = NaN, which the scan treats as quiet).
+template <int NPL>
+__host__ __device__ constexpr int qkp_nbp() {
+  return ((NPL + 2) + 3) & ~3;
+}
 template <int NPL>
 __host__ __device__ constexpr int qkp_warp_smem_bytes() {
-  return ((NPL + 2) * 32 * 4 + (int)sizeof(WarpState) + 15) & ~15;
+  return (2 * qkp_nbp<NPL>() * 32 * 4 + (int)sizeof(WarpState) + 15) & ~15;
 }
 
-// Shared memory: [instance blob: Q rows | A_ext | c] [per warp: phi (NPL+2)*32 floats | WarpState]
+// Shared memory: [instance blob: Q rows | A_ext (NaN-padded) | c]
+//                [per warp: phs = (2x-1) phi | asg = (2x-1) A, each NBP*32 floats | WarpState]
 template <int NPL, int QB>
 __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunArgs a) {
   constexpr int E = 4 / QB;                          // Q entries per 32-bit word
   constexpr int QW = (NPL + E - 1) / E;              // words per lane per Q row
+  constexpr int NBP = qkp_nbp<NPL>();
+  constexpr float kQBias = (float)(1 << (8 * QB - 1));
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t mbar;
 
@@ -128,25 +119,32 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   if (ridx >= a.R) return;
   const InstHdr *Hp = a.hdr + s;
   const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem) + lane;       // Q word (row 0, w 0) of this lane
-  const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane] (0-padded)
+  const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane] (NaN-padded)
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + a.c_off);
   unsigned char *wbase = smem + a.blob_bytes + warp * qkp_warp_smem_bytes<NPL>();
-  float *phw = reinterpret_cast<float *>(wbase) + lane;                        // phi[32b + lane], 0 beyond items
-  WarpState *ws = reinterpret_cast<WarpState *>(wbase + (NPL + 2) * 32 * 4);
+  float *phs = reinterpret_cast<float *>(wbase) + lane;                        // (2x_i - 1) phi_i, i = 32b + lane
+  float *asg = reinterpret_cast<float *>(wbase) + NBP * 32 + lane;             // (2x_i - 1) A_i
+  WarpState *ws = reinterpret_cast<WarpState *>(wbase + 2 * NBP * 32 * 4);
   const int n = a.n;
   const int N = Hp->N;
   const int NB = (N + 31) >> 5;                      // NB <= NPL + 2
+  const int NG = (NB + 3) >> 2;
   const bool has_con = a.M > 0;
 
+  // x = 0: phi_i = -c_i, so (2x-1) phi = c_i; (2x-1) A = -A.
 #pragma unroll
-  for (int m = 0; m < NPL + 2; ++m) phw[32 * m] = (32 * m + lane < n) ? (float)(-sC[32 * m + lane]) : 0.0f;  // x = 0
+  for (int m = 0; m < NBP; ++m) {
+    phs[32 * m] = (32 * m + lane < n) ? (float)sC[32 * m + lane] : 0.0f;
+    asg[32 * m] = -sAl[32 * m];
+  }
   if (lane == 0) {
-    ws->bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
-    ws->k1step = ws->bstep * Hp->c_o;
-    ws->k2step = ws->bstep * Hp->c_p;
-    ws->k3step = 0.0;
-    ws->e0step = ws->bstep * Hp->c_o * Hp->phi_bound * 0x1p-20;
-    ws->e1step = ws->bstep * Hp->c_p * Hp->v_bound * 0x1p-20;
+    const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
+    ws->bstep = bstep;
+    ws->k1s = (float)(bstep * Hp->c_o);
+    ws->k2s = (float)(bstep * Hp->c_p);
+    ws->k3s = 0.0f;
+    ws->e0s = (float)(bstep * Hp->c_o * Hp->phi_bound * 0x1p-20);
+    ws->e1s = (float)(bstep * Hp->c_p * Hp->v_bound * 0x1p-20);
     ws->Lam = 0;
     ws->best_f = LLONG_MAX;
     ws->best_k = -1;
@@ -163,11 +161,33 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)(a.rep0 + ridx);
 
   // Flip of spin j = 32b + L by delta = dl (+1/-1): Eq. 9 in incremental form.
+  //   own lane: x_j, and the signs of its (2x-1) phi, (2x-1) A;  all lanes: phi_i -= delta Q_ij
+  //   (stored as (2x_i - 1) phi_i), r += delta A_j.
   auto apply_flip = [&](int b, int L, float AL, float dl) {
     r2 = fmaf(dl + dl, AL, r2);
-    if (lane == L) xm ^= (1u << b);
+    if (lane == L) {
+      xm ^= (1u << b);
+      phs[32 * b] = -phs[32 * b];
+      asg[32 * b] = -asg[32 * b];
+    }
     const int j = 32 * b + L;
-    if (j < n) phi_update<NPL, QB>(sQl + j * (QW * 32), phw, dl);
+    if (j < n) {
+      const uint32_t *row = sQl + j * (QW * 32);
+#pragma unroll
+      for (int w = 0; w < QW; ++w) {
+        const uint32_t word = row[32 * w];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int m = E * w + e;
+          if (m < NPL) {
+            const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
+            const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
+            const float sdl = ((xm >> m) & 1u) ? dl : -dl;           // (2x_i - 1) delta
+            phs[32 * m] = fmaf(-sdl, q, phs[32 * m]);
+          }
+        }
+      }
+    }
     cnt_add(ws, kCntFlips, 1);
   };
 
@@ -176,7 +196,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (a.T >= 2) {
       // ---- sweep t = 0: beta_0 = 0, x_i = [u < 1/2] (state-independent; R3, R5) ----
       t0 = 1;
-      for (int g = 0; 4 * g < NB; ++g) {
+      for (int g = 0; g < NG; ++g) {
         const uint4 uw = philox_group(key, g, lane, 0, k, srho);
         cnt_add(ws, kCntPhilox, 32);
 #pragma unroll
@@ -200,127 +220,111 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     }
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
     for (int t = t0; t < a.T; ++t) {
-      const double tt = (a.T >= 2) ? (double)t : 1.0;
+      const float tf = (a.T >= 2) ? (float)t : 1.0f;     // exact
       bool active = false;                            // any non-quiet lane in this sweep?
-      const float K1 = (float)(tt * ws->k1step), K2 = (float)(tt * ws->k2step), K3 = (float)(tt * ws->k3step);
-      // Scan threshold: quiet <=> +-z_f32 > kSatThr + tt*(e0step + e1step*A), where the second term
+      // fp32 sweep constants (two roundings each; the bounds below keep a >= 3x margin)
+      const float K1 = tf * ws->k1s, K2 = tf * ws->k2s, K3 = tf * ws->k3s;
+      // Scan threshold: quiet <=> (2x-1) z_f32 > kSatThr + t*(e0s + e1s*A), where the second term
       // bounds |z_f32 - z| for every reachable state (phi_bound, v_bound; 4x margin over 3*2^-24).
-      const float B0 = kSatThr + (float)(tt * ws->e0step) * 1.0001f;
-      const float B1 = (float)(tt * ws->e1step) * 1.0001f;
+      const float B0 = fmaf(tf, ws->e0s, kSatThr), B1 = tf * ws->e1s;
       int g = 0;                                          // current 128-spin group (4 blocks)
-      int nbg = 4;                                        // blocks in group g
       uint4 uw = make_uint4(0, 0, 0, 0);                  // group g's uniforms, drawn lazily
       bool have_u = false;
 
-        // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
-        // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
-        // Returns true if a spin of the block flipped.
-        auto process_block = [&](int b, int bb) -> bool {
-          const int hi = N - 32 * b;                      // lanes < hi hold a spin
-          const float A = sAl[32 * b];
-          const bool xb = (xm >> b) & 1u;
-          const float sg = xb ? -1.0f : 1.0f;            // v = 2 r0 + A = 2r + A (1 - 2 x_i)
-          const float sq = xb ? kZScale : -kZScale;       // "quiet" direction: z > 0 keeps x = 1
-          const float AK2 = A * K2, AK3 = A * K3;
-          bool flipped = false;
-          int lo = 0;                                     // lanes in [lo, hi) are still pending
-          for (;;) {
-            const float phib = phw[32 * b];
-            const float v = fmaf(A, sg, r2);
-            const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));            // beta_t F_i (fp32)
-            const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
-            const bool mine = lane >= lo && lane < hi;
-            const bool sat = fabsf(z) * kZScale - S > kSatThr20;
-            int nx = z > 0.0f;
-            const uint32_t need = __ballot_sync(kFull, mine && !sat);
-            if (need) {
-              if (!have_u) {
-                uw = philox_group_lazy(key, g, lane, t, k, srho);
-                have_u = true;
-                cnt_add(ws, kCntPhilox, 32);
-              }
-              cnt_add(ws, kCntUnif, __popc(need));
-              if (mine && !sat) {
-                const uint32_t w = sel4(uw, bb);
-                const float l = logit_f32(w);
-                const float d = z - l;
-                const float el = kLogitAbs + kLogitRel * fabsf(l);
-                if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
-                  nx = d > 0.0f;
-                } else {
-                  const int rs = decide_fp64(phib, v, A, a.T >= 2 ? t : 1, Hp, ws, w);
-                  nx = rs & 1;
-                  atomicAdd(&ws->cnt[kCntFp64], 1u);
-                  if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
-                }
+      // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
+      // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
+      // Returns true if a spin of the block flipped.
+      auto process_block = [&](int b, int bb) -> bool {
+        const int hi = N - 32 * b;                        // lanes < hi hold a spin
+        const float A = sAl[32 * b];
+        const bool xb = (xm >> b) & 1u;
+        const float AK2 = A * K2, AK3 = A * K3;
+        const float sg = xb ? -1.0f : 1.0f;              // 1 - 2x_i
+        bool flipped = false;
+        int lo = 0;                                       // lanes in [lo, hi) are still pending
+        for (;;) {
+          const float phib = -sg * phs[32 * b];           // phi_i
+          const float v = fmaf(A, sg, r2);                // 2 r0 + A
+          const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));            // beta_t F_i (fp32)
+          const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
+          const bool mine = lane >= lo && lane < hi;
+          const bool sat = fabsf(z) * kZScale - S > kSatThr20;
+          int nx = z > 0.0f;
+          const uint32_t need = __ballot_sync(kFull, mine && !sat);
+          if (need) {
+            if (!have_u) {
+              uw = philox_group_lazy(key, g, lane, t, k, srho);
+              have_u = true;
+              cnt_add(ws, kCntPhilox, 32);
+            }
+            cnt_add(ws, kCntUnif, __popc(need));
+            if (mine && !sat) {
+              const uint32_t w = sel4(uw, bb);
+              const float l = logit_f32(w);
+              const float d = z - l;
+              const float el = kLogitAbs + kLogitRel * fabsf(l);
+              if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
+                nx = d > 0.0f;
+              } else {
+                const int rs = decide_fp64(phib, v, A, a.T >= 2 ? t : 1, Hp, ws, w);
+                nx = rs & 1;
+                atomicAdd(&ws->cnt[kCntFp64], 1u);
+                if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
               }
             }
-            const uint32_t fm = __ballot_sync(kFull, mine && nx != (int)xb);
-            if (!fm) break;
-            const int L = __ffs(fm) - 1;
-            apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
-            flipped = true;
-            lo = L + 1;
-            if (lo >= hi) break;
-            (void)sq;
           }
-          return flipped;
-        };
+          const uint32_t fm = __ballot_sync(kFull, mine && nx != (int)xb);
+          if (!fm) break;
+          const int L = __ffs(fm) - 1;
+          apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+          flipped = true;
+          lo = L + 1;
+          if (lo >= hi) break;
+        }
+        return flipped;
+      };
 
-        // Speculative scan of group g's blocks bb >= bstart on the current state: bit bb of the
-        // result is set if this lane's spin in block bb is not certified quiet (saturated towards
-        // its current value).  zz = +-z (sign of x_i): quiet <=> zz > B0 + B1*A (see B0, B1).
-        auto scan_one = [&](uint32_t &nq, int b, int bb, bool check_valid) {
-          const float A = sAl[32 * b];
-          const float ph = phw[32 * b];
-          const bool xb = (xm >> b) & 1u;
-          const float Asg = xb ? A : -A;                   // -(A (1 - 2x_i))
-          const float v = r2 - Asg;                        // 2 r0 + A
-          const float tq = fmaf(K2, v, K3);
-          const float zz = fmaf(xb ? K1 : -K1, ph, -(Asg * tq));   // (2x_i - 1) * z
-          const bool quiet = zz > fmaf(B1, A, B0);
-          if (!quiet && (!check_valid || lane < N - 32 * b)) nq |= 1u << bb;
-        };
-        auto scan_general = [&](int bstart) -> uint32_t {
+      // Speculative scan of one block on the current state: bit bb of nq is set if this lane's
+      // spin is not certified quiet (saturated towards its current value).  With zz = (2x-1) z:
+      //   zz = K1 (2x-1)phi - (2x-1)A (K2 v + K3),  v = 2r - (2x-1)A  = 2 r0 + A,
+      //   quiet <=> zz > B0 + B1 |A|;  NaN padding (spins >= N) compares false -> quiet.
+      auto scan_one = [&](uint32_t &nq, int b, int bb) {
+        const float as = asg[32 * b];
+        const float ph = phs[32 * b];
+        const float v = r2 - as;
+        const float tq = fmaf(K2, v, K3);
+        const float zz = fmaf(K1, ph, -(as * tq));
+        if (zz <= fmaf(B1, fabsf(as), B0)) nq |= 1u << bb;
+      };
+      // Process the non-quiet blocks of group g in order (exactly); after a flip the later
+      // blocks' speculation is stale, so they are rescanned.
+      auto handle_group = [&](uint32_t m) {
+        active = true;
+        for (;;) {
+          int bstart = 4;
+          while (m) {
+            const int bb = __ffs(m) - 1;
+            m &= m - 1u;
+            if (process_block(4 * g + bb, bb)) { bstart = bb + 1; break; }
+          }
+          if (bstart >= 4) return;
           uint32_t nq = 0;
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb)
-            if (bb >= bstart && bb < nbg) scan_one(nq, 4 * g + bb, bb, true);
-          return __reduce_or_sync(kFull, nq);
-        };
-        // Process the non-quiet blocks of group g in order (exactly); after a flip the later
-        // blocks' speculation is stale, so they are rescanned.
-        auto handle_group = [&](uint32_t m) {
-          active = true;
-          for (;;) {
-            int bstart = 4;
-            while (m) {
-              const int bb = __ffs(m) - 1;
-              m &= m - 1u;
-              if (process_block(4 * g + bb, bb)) { bstart = bb + 1; break; }
-            }
-            if (bstart >= nbg) return;
-            m = scan_general(bstart);
-            if (!m) return;
-          }
-        };
+            if (bb >= bstart) scan_one(nq, 4 * g + bb, bb);
+          m = __reduce_or_sync(kFull, nq);
+          if (!m) return;
+        }
+      };
 
-        const int NGF = N >> 7;                           // groups of four full blocks
-        for (g = 0; g < NGF; ++g) {                       // hot path
-          have_u = false;
-          nbg = 4;
-          uint32_t nq = 0;
+      for (g = 0; g < NG; ++g) {
+        have_u = false;
+        uint32_t nq = 0;
 #pragma unroll
-          for (int bb = 0; bb < 4; ++bb) scan_one(nq, 4 * g + bb, bb, false);
-          const uint32_t m = __reduce_or_sync(kFull, nq);
-          if (m) handle_group(m);
-        }
-        for (; 4 * g < NB; ++g) {                         // the ragged tail group
-          have_u = false;
-          nbg = min(4, NB - 4 * g);
-          const uint32_t m = scan_general(0);
-          if (m) handle_group(m);
-        }
+        for (int bb = 0; bb < 4; ++bb) scan_one(nq, 4 * g + bb, bb);
+        const uint32_t m = __reduce_or_sync(kFull, nq);
+        if (m) handle_group(m);
+      }
       cnt_add(ws, kCntSweeps, 1);
       // Frozen anneal: a sweep in which every spin was certified
       // saturated towards its current value changed nothing; fields stay constant and beta only
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #pragma unroll
     for (int m = 0; m < NPL; ++m) {
       if (((xm >> m) & 1u) && 32 * m + lane < n) {
-        fpart += sC[32 * m + lane] - (int)phw[32 * m];      // x_i (c_i - phi_i)
+        fpart += sC[32 * m + lane] - (int)phs[32 * m];      // x_i (c_i - phi_i); phs = phi when x_i = 1
         load += (int)sAl[32 * m];
       }
     }
@@ -368,9 +372,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     }
     __syncwarp();
     if (lane == 0) {                                  // lambda_{k+1} = lambda_k + eta g(x_k)  (R10)
+      const double Lnew = (double)(Lam + rl);
       ws->Lam = Lam + rl;
-      ws->k3step = ws->bstep * (Hp->c_l * (double)(Lam + rl));
-      ws->e1step = ws->bstep * (Hp->c_p * Hp->v_bound + Hp->c_l * fabs((double)(Lam + rl))) * 0x1p-20;
+      ws->k3s = (float)(ws->bstep * (Hp->c_l * Lnew));
+      ws->e1s = (float)(ws->bstep * (Hp->c_p * Hp->v_bound + Hp->c_l * fabs(Lnew)) * 0x1p-20);
     }
     __syncwarp();
   }
