@@ -289,6 +289,14 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
         brow[k] = prob->b[(size_t)s * M + k];
         qrow[k] = ctx->q[s][k];
       }
+      float *band = reinterpret_cast<float *>(B + L.band);
+      band[0] = 0.0f;
+      for (int i = 1; i < n; ++i) {
+        double g = 0.0;
+        for (int k = 0; k < M; ++k)
+          g += (double)prob->A[((size_t)s * M + k) * n + i] * (double)prob->A[((size_t)s * M + k) * n + i - 1];
+        band[i] = (float)g;
+      }
     }
   } else {
     delete ctx;

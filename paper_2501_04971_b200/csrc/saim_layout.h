@@ -49,8 +49,10 @@ inline __host__ __device__ uint32_t align16u(uint32_t v) { return (v + 15u) & ~1
 //   cint   int32 [n]       c_i (exact objective for the readout)
 //   brow   int64 [MM]      b_m
 //   qrow   int32 [MM]      slack bit count q_m (0 for padded rows)
+//   band   float [n]       G_i = A_{.i} . A_{.i-1} (adjacent item columns; G_0 = 0) -- the O(n)
+//                          band used by the one-spin lookahead, not the dense A^T A
 struct MkpLayout {
-  uint32_t acol, iconst, cint, brow, qrow, bytes;
+  uint32_t acol, iconst, cint, brow, qrow, band, bytes;
 };
 inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
   MkpLayout L;
@@ -60,6 +62,7 @@ inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
   L.cint = o;   o += align16u((uint32_t)n * 4u);
   L.brow = o;   o += (uint32_t)MM * 8u;
   L.qrow = o;   o += align16u((uint32_t)MM * 4u);
+  L.band = o;   o += align16u((uint32_t)n * 4u);
   L.bytes = o;
   return L;
 }

@@ -83,6 +83,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
   const double c_o = Hp->c_o, c_p = Hp->c_p, c_l = Hp->c_l;
   const float twocp = (float)(2.0 * c_p), cpf = (float)c_p;
   const float rbound = (float)Hp->r_bound;
+  const float amax = (float)(Hp->v_bound - 2.0 * Hp->r_bound);   // max A_ext entry
+  const float *sBand = reinterpret_cast<const float *>(smem + L.band);
 
   float r[MM], cL[MM];
 #pragma unroll
@@ -108,9 +110,10 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       cL[m] = (float)(c_l * (double)Lam[32 * m]);
       cLmax = fmaxf(cLmax, fabsf(cL[m]));
     }
-    // |z_f32 - z| <= beta (E1 |A_i|_1 + E0_i) + 2^-23 |z|, E = (MM+6) 2^-24 (...);
-    // the factor 2 below is a safety margin.
-    const float E1 = (float)((MM + 6) * 0x1p-24 * (2.0 * c_p * (double)rbound + (double)cLmax)) * 2.0f;
+    // |z_f32 - z| <= beta (E1 |A_i|_1 + E0_i) + 2^-23 |z|, E = (MM+8) 2^-24 (...):
+    // the lookahead's band value adds |A_i . A_{i-1}| <= |A_i|_1 max A; factor 2: safety margin.
+    const float E1 =
+        (float)((MM + 8) * 0x1p-24 * (2.0 * c_p * ((double)rbound + (double)amax) + (double)cLmax)) * 2.0f;
 
     for (int t = 0; t < a.T; ++t) {
       const bool bz = (a.T >= 2) && (t == 0);          // beta_0 = 0: x_i = [u < 1/2]
@@ -147,12 +150,11 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         return rs & 1;
       };
 
-      // ---- items i = 0..n-1 ----
-      for (int i = 0; i < n; ++i) {
-        if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
-        if ((i & 127) == 0) fill_group(i >> 7);
-        const float l = lt[32 * (i & 127)];
-        const int xb = (xcur >> (i & 31)) & 1u;
+      // ---- items i = 0..n-1, with a one-spin lookahead ----
+      // pre = A_i . r evaluated with r as it was BEFORE the decision of spin i-1 (so it is computed
+      // off the sequential dependency chain, during step i-1); the exact dot follows from one fma
+      // with the band value G_i = A_i . A_{i-1}:  A_i . r_now = pre + delta_{i-1} G_i.
+      auto dots = [&](int i, float &pr, float &dlv) {
         const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
         float dr0 = 0.f, dr1 = 0.f, dl0 = 0.f, dl1 = 0.f;
 #pragma unroll
@@ -163,26 +165,44 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1);
           dl0 = fmaf(av.z, cL[4 * m4 + 2], dl0); dl1 = fmaf(av.w, cL[4 * m4 + 3], dl1);
         }
+        pr = dr0 + dr1;
+        dlv = dl0 + dl1;
+      };
+      float pre = 0.f, dlc = 0.f, dprev = 0.f, Gc = 0.f;
+      if (n > 0) dots(0, pre, dlc);
+      for (int i = 0; i < n; ++i) {
+        if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
+        if ((i & 127) == 0) fill_group(i >> 7);
+        const float l = lt[32 * (i & 127)];
+        const int xb = (xcur >> (i & 31)) & 1u;
+        const float dr = fmaf(dprev, Gc, pre);           // A_i . r (current state)
+        // lookahead for spin i+1 (independent of this step's decision)
+        float pre_n = 0.f, dl_n = 0.f, G_n = 0.f;
+        if (i + 1 < n) {
+          dots(i + 1, pre_n, dl_n);
+          G_n = sBand[i + 1];
+        }
         const float4 ic = sIc[i];                        // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
         const float sg = xb ? -1.0f : 1.0f;              // 1 - 2 x_i
-        const float F = fmaf(-twocp, dr0 + dr1, fmaf(-ic.y, sg, ic.x)) - (dl0 + dl1);
+        const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
         const float z = bf * F;
         const float e = bf * fmaf(E1, ic.z, ic.w) + fabsf(z) * 0x1p-22f;
         const int nx = decide(z, e, l, [&]() -> int {
           const uint32_t w = word_of(key, i, t, k, srho);
-          double dr = 0.0, dl = 0.0, a2 = 0.0;
+          double drd = 0.0, dld = 0.0, a2 = 0.0;
 #pragma unroll
           for (int m = 0; m < MM; ++m) {
             const double Am = (double)sAcol[i * MM + m];
-            dr += Am * (double)r[m];
-            dl += Am * (double)Lam[32 * m];
+            drd += Am * (double)r[m];
+            dld += Am * (double)Lam[32 * m];
             a2 += Am * Am;
           }
-          const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * dr, t4 = c_l * dl;
+          const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * drd, t4 = c_l * dld;
           const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
           return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), w);
         });
         const float dl = (float)(nx - xb);                  // delta in {-1, 0, +1}; fma(0, A, r) == r
+        const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
 #pragma unroll
         for (int m4 = 0; m4 < MM / 4; ++m4) {
           const float4 av = Ac[m4];
@@ -193,6 +213,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         }
         if (nx != xb) { xcur ^= 1u << (i & 31); ++c_flips; }
         if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
+        pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
       }
       // ---- slack bits: row m, bit q, spin i = n + sum_{m'<m} q_m' + q (R4) ----
       int i = n;
