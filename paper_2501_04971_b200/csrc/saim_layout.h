@@ -57,12 +57,12 @@ struct MkpLayout {
 inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
   MkpLayout L;
   uint32_t o = 0;
-  L.acol = o;   o += align16u((uint32_t)n * MM * 4u);
+  L.acol = o;   o += align16u((uint32_t)(n + 1) * MM * 4u);     // + one zero column (lookahead past n-1)
   L.iconst = o; o += (uint32_t)n * 16u;
   L.cint = o;   o += align16u((uint32_t)n * 4u);
   L.brow = o;   o += (uint32_t)MM * 8u;
   L.qrow = o;   o += align16u((uint32_t)MM * 4u);
-  L.band = o;   o += align16u((uint32_t)n * 4u);
+  L.band = o;   o += align16u((uint32_t)(n + 1) * 4u);
   L.bytes = o;
   return L;
 }

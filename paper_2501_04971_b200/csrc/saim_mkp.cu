@@ -137,17 +137,25 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         c_philox += 32;
       };
       // Certified decision [u < sigma(z)] (R18, R19) from z, its error bound e and l = logit(u)
-      // (exact sign); slow(): fp64 re-evaluation returning (x | uncertified << 1).
+      // (exact sign), evaluated branch-free; only the rare fp64 re-evaluation (slow(): returns
+      // x | uncertified << 1) sits behind a warp vote.
       auto decide = [&](float z, float e, float l, auto slow) -> int {
-        if (bz) return (int)(__float_as_uint(l) >> 31);  // beta_0 = 0: u < 1/2 (sign bit, -0 included)
-        if (fabsf(z) - e > kSatThr) return z > 0.0f;
-        ++c_unif;
+        const bool sat = fabsf(z) - e > kSatThr;
         const float d = z - l;
-        if (fabsf(d) > (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f) return d > 0.0f;
-        ++c_fp64;
-        const int rs = slow();
-        if (rs & 2) ++c_unc;
-        return rs & 1;
+        const bool cert = fabsf(d) > (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f;
+        int nx = sat ? (z > 0.0f) : (d > 0.0f);
+        if (bz) nx = (int)(__float_as_uint(l) >> 31);     // beta_0 = 0: u < 1/2 (sign bit, -0 included)
+        c_unif += (!bz && !sat) ? 1u : 0u;
+        const bool need = !bz && !sat && !cert;
+        if (__any_sync(kFull, need)) {
+          if (need) {
+            ++c_fp64;
+            const int rs = slow();
+            if (rs & 2) ++c_unc;
+            nx = rs & 1;
+          }
+        }
+        return nx;
       };
 
       // ---- items i = 0..n-1, with a one-spin lookahead ----
@@ -169,54 +177,57 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         dlv = dl0 + dl1;
       };
       float pre = 0.f, dlc = 0.f, dprev = 0.f, Gc = 0.f;
-      if (n > 0) dots(0, pre, dlc);
-      for (int i = 0; i < n; ++i) {
-        if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
-        if ((i & 127) == 0) fill_group(i >> 7);
-        const float l = lt[32 * (i & 127)];
-        const int xb = (xcur >> (i & 31)) & 1u;
-        const float dr = fmaf(dprev, Gc, pre);           // A_i . r (current state)
-        // lookahead for spin i+1 (independent of this step's decision)
-        float pre_n = 0.f, dl_n = 0.f, G_n = 0.f;
-        if (i + 1 < n) {
-          dots(i + 1, pre_n, dl_n);
-          G_n = sBand[i + 1];
-        }
-        const float4 ic = sIc[i];                        // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
-        const float sg = xb ? -1.0f : 1.0f;              // 1 - 2 x_i
-        const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
-        const float z = bf * F;
-        const float e = bf * fmaf(E1, ic.z, ic.w) + fabsf(z) * 0x1p-22f;
-        const int nx = decide(z, e, l, [&]() -> int {
-          const uint32_t w = word_of(key, i, t, k, srho);
-          double drd = 0.0, dld = 0.0, a2 = 0.0;
+      dots(0, pre, dlc);                                  // (column n is zero: the lookahead past n-1 is harmless)
+      for (int w = 0; 32 * w < n; ++w) {
+        xcur = xw[32 * w];
+        if ((w & 3) == 0) fill_group(w >> 2);
+        const int iend = min(32, n - 32 * w);
+        for (int ii = 0; ii < iend; ++ii) {
+          const int i = 32 * w + ii;
+          const float l = lt[32 * (i & 127)];
+          const int xb = (xcur >> ii) & 1u;
+          const float dr = fmaf(dprev, Gc, pre);          // A_i . r (current state)
+          float pre_n, dl_n;
+          dots(i + 1, pre_n, dl_n);                       // lookahead (independent of this decision)
+          const float G_n = sBand[i + 1];
+          const float4 ic = sIc[i];                       // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
+          const float sg = xb ? -1.0f : 1.0f;             // 1 - 2 x_i
+          const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
+          const float z = bf * F;
+          const float e = bf * fmaf(E1, ic.z, ic.w) + fabsf(z) * 0x1p-22f;
+          const int nx = decide(z, e, l, [&]() -> int {
+            const uint32_t wd = word_of(key, i, t, k, srho);
+            double drd = 0.0, dld = 0.0, a2 = 0.0;
 #pragma unroll
-          for (int m = 0; m < MM; ++m) {
-            const double Am = (double)sAcol[i * MM + m];
-            drd += Am * (double)r[m];
-            dld += Am * (double)Lam[32 * m];
-            a2 += Am * Am;
+            for (int m = 0; m < MM; ++m) {
+              const double Am = (double)sAcol[i * MM + m];
+              drd += Am * (double)r[m];
+              dld += Am * (double)Lam[32 * m];
+              a2 += Am * Am;
+            }
+            const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * drd, t4 = c_l * dld;
+            const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
+            return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), wd);
+          });
+          const float dl = (float)(nx - xb);              // delta in {-1, 0, +1}; fma(0, A, r) == r
+          const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
+#pragma unroll
+          for (int m4 = 0; m4 < MM / 4; ++m4) {
+            const float4 av = Ac[m4];
+            r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
+            r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
+            r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
+            r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
           }
-          const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * drd, t4 = c_l * dld;
-          const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
-          return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), w);
-        });
-        const float dl = (float)(nx - xb);                  // delta in {-1, 0, +1}; fma(0, A, r) == r
-        const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
-#pragma unroll
-        for (int m4 = 0; m4 < MM / 4; ++m4) {
-          const float4 av = Ac[m4];
-          r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
-          r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
-          r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
-          r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
+          xcur ^= (uint32_t)(nx != xb) << ii;
+          c_flips += (nx != xb) ? 1u : 0u;
+          pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
         }
-        if (nx != xb) { xcur ^= 1u << (i & 31); ++c_flips; }
-        if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
-        pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
+        xw[32 * w] = xcur;
       }
       // ---- slack bits: row m, bit q, spin i = n + sum_{m'<m} q_m' + q (R4) ----
       int i = n;
+      xcur = xw[32 * (n >> 5)];                            // word holding spin n (stored by the item loop)
 #pragma unroll
       for (int m = 0; m < MM; ++m) {
         const int qm = (m < M) ? sQ[m] : 0;
@@ -240,11 +251,9 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
             const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
             return certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
           });
-          if (nx != xb) {
-            r[m] = fmaf((float)(nx - xb), A, r[m]);
-            xcur ^= 1u << (i & 31);
-            ++c_flips;
-          }
+          r[m] = fmaf((float)(nx - xb), A, r[m]);
+          xcur ^= (uint32_t)(nx != xb) << (i & 31);
+          c_flips += (nx != xb) ? 1u : 0u;
           if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
         }
       }
