@@ -182,15 +182,19 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         xcur = xw[32 * w];
         if ((w & 3) == 0) fill_group(w >> 2);
         const int iend = min(32, n - 32 * w);
+        // state-independent operands of the current step, prefetched one step ahead
+        float l = lt[32 * ((32 * w) & 127)];
+        float4 ic = sIc[32 * w];                          // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
+        float G_n = sBand[32 * w + 1];
         for (int ii = 0; ii < iend; ++ii) {
           const int i = 32 * w + ii;
-          const float l = lt[32 * (i & 127)];
+          const float l_n = lt[32 * ((i + 1) & 127)];     // valid for ii + 1 < iend (same group)
+          const float4 ic_n = sIc[i + 1];                 // padded entry n
+          const float G_nn = sBand[i + 2 <= n ? i + 2 : n];
           const int xb = (xcur >> ii) & 1u;
           const float dr = fmaf(dprev, Gc, pre);          // A_i . r (current state)
           float pre_n, dl_n;
           dots(i + 1, pre_n, dl_n);                       // lookahead (independent of this decision)
-          const float G_n = sBand[i + 1];
-          const float4 ic = sIc[i];                       // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
           const float sg = xb ? -1.0f : 1.0f;             // 1 - 2 x_i
           const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
           const float z = bf * F;
@@ -222,6 +226,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           xcur ^= (uint32_t)(nx != xb) << ii;
           c_flips += (nx != xb) ? 1u : 0u;
           pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
+          l = l_n; ic = ic_n; G_n = G_nn;
         }
         xw[32 * w] = xcur;
       }
