@@ -16,6 +16,7 @@
 // slow path (counted when even that is not certain).
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 
 #include "saim_dev.cuh"
 
@@ -125,15 +126,22 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // (32g + j, t, k, s<<20|rho) yields the words of spins 128g + 32w + j, w = 0..3).  They do
       // not depend on the state, so they are drawn in one ILP-friendly burst per group, off the
       // sequential dependency chain of the decisions.
-      auto fill_group = [&](int g) {
+      auto fill_words = [&](int g, auto NW) {              // NW = words of the group holding spins
 #pragma unroll 4
         for (int j = 0; j < 32; ++j) {
           const uint4 w4 = philox_group(key, g, j, t, k, srho);
           lt[32 * (j + 0)] = logit_signed(w4.x);
-          lt[32 * (j + 32)] = logit_signed(w4.y);
-          lt[32 * (j + 64)] = logit_signed(w4.z);
-          lt[32 * (j + 96)] = logit_signed(w4.w);
+          if (NW.value > 1) lt[32 * (j + 32)] = logit_signed(w4.y);
+          if (NW.value > 2) lt[32 * (j + 64)] = logit_signed(w4.z);
+          if (NW.value > 3) lt[32 * (j + 96)] = logit_signed(w4.w);
         }
+      };
+      auto fill_group = [&](int g) {
+        const int nw = min(4, (N - 128 * g + 31) >> 5);
+        if (nw >= 4) fill_words(g, std::integral_constant<int, 4>{});
+        else if (nw == 3) fill_words(g, std::integral_constant<int, 3>{});
+        else if (nw == 2) fill_words(g, std::integral_constant<int, 2>{});
+        else fill_words(g, std::integral_constant<int, 1>{});
         c_philox += 32;
       };
       // Certified decision [u < sigma(z)] (R18, R19) from z, its error bound e and l = logit(u)
