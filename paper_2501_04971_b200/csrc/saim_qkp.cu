@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         const float AK2 = A * K2, AK3 = A * K3;
         const float sg = xb ? -1.0f : 1.0f;              // 1 - 2x_i
         bool flipped = false;
+        bool have_l = false;                              // logit of this lane's u, drawn once per visit
+        float l = 0.0f, el = 0.0f;
+        uint32_t w = 0;
         int lo = 0;                                       // lanes in [lo, hi) are still pending
         for (;;) {
           const float phib = -sg * phs[32 * b];           // phi_i
@@ -252,17 +255,20 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           int nx = z > 0.0f;
           const uint32_t need = __ballot_sync(kFull, mine && !sat);
           if (need) {
-            if (!have_u) {
-              uw = philox_group_lazy(key, g, lane, t, k, srho);
-              have_u = true;
-              cnt_add(ws, kCntPhilox, 32);
+            if (!have_l) {
+              if (!have_u) {
+                uw = philox_group_lazy(key, g, lane, t, k, srho);
+                have_u = true;
+                cnt_add(ws, kCntPhilox, 32);
+              }
+              w = sel4(uw, bb);
+              l = logit_f32(w);
+              el = kLogitAbs + kLogitRel * fabsf(l);
+              have_l = true;
             }
             cnt_add(ws, kCntUnif, __popc(need));
             if (mine && !sat) {
-              const uint32_t w = sel4(uw, bb);
-              const float l = logit_f32(w);
               const float d = z - l;
-              const float el = kLogitAbs + kLogitRel * fabsf(l);
               if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
                 nx = d > 0.0f;
               } else {
