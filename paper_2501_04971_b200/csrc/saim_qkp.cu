@@ -58,12 +58,11 @@ struct WarpState {
   int best_k, nfeas;
   uint32_t cnt[7];                 // flips, uniforms, fp64, uncertified, philox, sweeps evaluated, groups skipped
   uint32_t best_word[32];
-  // Group skip (DESIGN.md 6.1 "Quiet-group certificates"): H[g] = gm (1 - 2^-18) + 1.01 dacc_0,
-  // gm = min over the group's lanes of ((2x-1) z - e)/t at its last quiet scan (field units per
-  // unit t), dacc_0 = the running bound dacc of |d(z/t)| caused by flips (this anneal) at that scan.
-  // The group is certified quiet at sweep t while 1.01 dacc + ln(2^24-1) (1 + 2^-18) / t < H[g].
-  float H[8];
-  float twok2amax;
+  // Group skip (DESIGN.md 6.1 "Quiet-group certificates"): gm = min over the group's lanes of
+  // (2x-1) z/t - e/t at its last quiet scan (field units per unit t), gd = dacc at that scan;
+  // dacc = running bound of |d(z/t)| caused by flips in this anneal.
+  float gm[8], gd[8];
+  float dacc, twok2amax;
 };
 enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps, kCntSkip };
 
@@ -163,7 +162,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   ws->best_word[lane] = 0;
   __syncwarp();
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
-  float dacc = 0.0f;                                // running field-change bound (warp-uniform)
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
   const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
@@ -174,8 +172,9 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   //   (stored as (2x_i - 1) phi_i), r += delta A_j.
   auto apply_flip = [&](int b, int L, float AL, float dl) {
     r2 = fmaf(dl + dl, AL, r2);
-    // |d(z_i/t)| <= k1 max_i|Q_ij| + 2 k2 A_max A_j (computed identically by every lane)
-    dacc += fmaf(ws->twok2amax, AL, ws->k1s * sQmax[32 * b + L]) * 1.01f;
+    if (lane == 0)                                    // |d(z_i/t)| <= k1 max_i|Q_ij| + 2 k2 A_max A_j
+      ws->dacc += fmaf(ws->twok2amax, AL, ws->k1s * sQmax[32 * b + L]) * 1.01f;
+    __syncwarp();
     if (lane == L) {
       xm ^= (1u << b);
       phs[32 * b] = -phs[32 * b];
@@ -230,9 +229,12 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
-    dacc = 0.0f;
+    if (lane == 0) {
+      ws->dacc = 0.0f;
 #pragma unroll
-    for (int gg = 0; gg < 8; ++gg) ws->H[gg] = -INFINITY;       // no certificate yet (same value from every lane)
+      for (int gg = 0; gg < 8; ++gg) ws->gm[gg] = -INFINITY;   // no certificate yet
+    }
+    __syncwarp();
     for (int t = t0; t < a.T; ++t) {
       const float tf = (a.T >= 2) ? (float)t : 1.0f;     // exact
       bool active = false;                            // any non-quiet lane in this sweep?
@@ -341,9 +343,9 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       };
 
       const float inv_t = 1.0f / tf;
-      const float sat_t = kSatThr * inv_t * (1.0f + 0x1p-18f);
       for (g = 0; g < NG; ++g) {
-        if (fmaf(1.01f, dacc, sat_t) < ws->H[g]) {       // certified quiet: no scan needed
+        // certified-quiet group: t (gm - (dacc - gd)) > ln(2^24-1) (1% and 2^-20 safety margins)
+        if (tf * (ws->gm[g] - 1.01f * (ws->dacc - ws->gd[g])) * (1.0f - 0x1p-20f) > kSatThr) {
           cnt_add(ws, kCntSkip, 1);
           continue;
         }
@@ -353,15 +355,18 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) scan_one(nq, mg, 4 * g + bb, bb);
         const uint32_t m = __reduce_or_sync(kFull, nq);
-        float Hg = -INFINITY;                             // margins unknown after processing
         if (m) {
           handle_group(m);
+          if (lane == 0) ws->gm[g] = -INFINITY;           // margins unknown after processing
         } else {
-          // every lane quiet: certificate from the group's minimum margin (non-negative here)
-          const float mb = __uint_as_float(__reduce_min_sync(kFull, __float_as_uint(fmaxf(mg, 0.0f))));
-          Hg = fmaf((mb + kSatThr) * inv_t, 1.0f - 0x1p-18f, 1.01f * dacc);
+          // every lane quiet: record the group's minimum margin (non-negative here)
+          const uint32_t mb = __reduce_min_sync(kFull, __float_as_uint(fmaxf(mg, 0.0f)));
+          if (lane == 0) {
+            ws->gm[g] = (__uint_as_float(mb) + kSatThr) * inv_t;
+            ws->gd[g] = ws->dacc;
+          }
         }
-        ws->H[g] = Hg;                                    // same value from every lane
+        __syncwarp();
       }
       cnt_add(ws, kCntSweeps, 1);
       // Frozen anneal: a sweep in which every spin was certified
