@@ -47,8 +47,7 @@ extern "C" {
 #define SAIM_CNT_UNCERTIFIED 5   /* decisions not certified even in fp64 (expected 0) */
 #define SAIM_CNT_FEASIBLE 6      /* feasible samples x_k */
 #define SAIM_CNT_PHILOX 7        /* Philox4x32-10 evaluations (per lane) */
-#define SAIM_CNT_GROUPS_SKIPPED 8 /* QKP kernel: 128-spin groups certified quiet without a scan */
-#define SAIM_NUM_COUNTERS 9
+#define SAIM_NUM_COUNTERS 8
 
 /* Problem batch: n_inst instances sharing (n_items, n_cons).  HOST pointers; copied by
  * saim_create (the caller may free them on return).  Row-major, instance-major. */

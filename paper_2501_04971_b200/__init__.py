@@ -18,8 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsaim.so")
 
 SAIM_OK, SAIM_EINVAL, SAIM_ERANGE, SAIM_ESMEM, SAIM_ECUDA, SAIM_EUNSUPPORTED, SAIM_ENOMEM = 0, -1, -2, -3, -4, -5, -6
-COUNTER_NAMES = ["decisions", "flips", "sweeps", "uniforms", "fp64", "uncertified", "feasible", "philox",
-                 "groups_skipped"]
+COUNTER_NAMES = ["decisions", "flips", "sweeps", "uniforms", "fp64", "uncertified", "feasible", "philox"]
 FLAG_NO_FREEZE_EXIT = 1
 EXPORTS = ["saim_create", "saim_run", "saim_get_info", "saim_get_instance", "saim_destroy",
            "saim_last_error", "saim_selftest"]
@@ -150,7 +149,7 @@ class Solver:
             "best_k": torch.empty((S, R), dtype=torch.int32, device=dev),
             "n_feasible": torch.empty((S, R), dtype=torch.int32, device=dev),
             "inst_best": torch.empty((S,), dtype=torch.int64, device=dev),
-            "counters": torch.empty((len(COUNTER_NAMES),), dtype=torch.int64, device=dev),
+            "counters": torch.empty((8,), dtype=torch.int64, device=dev),
         }
         if trace:
             out.update(tr_f=torch.empty((S, R, K), dtype=torch.int64, device=dev),

@@ -56,7 +56,7 @@ struct WarpState {
   long long Lam;                   // Lambda_k (Lambda_0 = 0)
   long long best_f;
   int best_k, nfeas;
-  uint32_t cnt[7];                 // flips, uniforms, fp64, uncertified, philox, sweeps evaluated, groups skipped
+  uint32_t cnt[6];                 // flips, uniforms, fp64, uncertified, philox, sweeps evaluated
   uint32_t best_word[32];
   // Group skip (DESIGN.md 6.1 "Quiet-group certificates"): gm = min over the group's lanes of
   // (2x-1) z/t - e/t at its last quiet scan (field units per unit t), gd = dacc at that scan;
@@ -64,7 +64,7 @@ struct WarpState {
   float gm[8], gd[8];
   float dacc, twok2amax;
 };
-enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps, kCntSkip };
+enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps };
 
 __device__ __forceinline__ void cnt_add(WarpState *ws, int i, uint32_t v) {
   if ((threadIdx.x & 31) == 0) ws->cnt[i] += v;      // warp-uniform events, counted once
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     ws->best_k = -1;
     ws->nfeas = 0;
 #pragma unroll
-    for (int i = 0; i < 7; ++i) ws->cnt[i] = 0;
+    for (int i = 0; i < 6; ++i) ws->cnt[i] = 0;
   }
   ws->best_word[lane] = 0;
   __syncwarp();
@@ -174,7 +174,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     r2 = fmaf(dl + dl, AL, r2);
     if (lane == 0)                                    // |d(z_i/t)| <= k1 max_i|Q_ij| + 2 k2 A_max A_j
       ws->dacc += fmaf(ws->twok2amax, AL, ws->k1s * sQmax[32 * b + L]) * 1.01f;
-    __syncwarp();
     if (lane == L) {
       xm ^= (1u << b);
       phs[32 * b] = -phs[32 * b];
@@ -232,7 +231,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (lane == 0) {
       ws->dacc = 0.0f;
 #pragma unroll
-      for (int gg = 0; gg < 8; ++gg) ws->gm[gg] = -INFINITY;   // no certificate yet
+      for (int gg = 0; gg < 8; ++gg) ws->gm[gg] = -1.0f;
     }
     __syncwarp();
     for (int t = t0; t < a.T; ++t) {
@@ -345,10 +344,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       const float inv_t = 1.0f / tf;
       for (g = 0; g < NG; ++g) {
         // certified-quiet group: t (gm - (dacc - gd)) > ln(2^24-1) (1% and 2^-20 safety margins)
-        if (tf * (ws->gm[g] - 1.01f * (ws->dacc - ws->gd[g])) * (1.0f - 0x1p-20f) > kSatThr) {
-          cnt_add(ws, kCntSkip, 1);
-          continue;
-        }
+        if (tf * (ws->gm[g] - 1.01f * (ws->dacc - ws->gd[g])) * (1.0f - 0x1p-20f) > kSatThr) continue;
         have_u = false;
         uint32_t nq = 0;
         float mg = INFINITY;
@@ -357,7 +353,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         const uint32_t m = __reduce_or_sync(kFull, nq);
         if (m) {
           handle_group(m);
-          if (lane == 0) ws->gm[g] = -INFINITY;           // margins unknown after processing
+          if (lane == 0) ws->gm[g] = -1.0f;               // margins unknown after processing
         } else {
           // every lane quiet: record the group's minimum margin (non-negative here)
           const uint32_t mb = __reduce_min_sync(kFull, __float_as_uint(fmaxf(mg, 0.0f)));
@@ -453,7 +449,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     atomicAdd(c + SAIM_CNT_FEASIBLE, (unsigned long long)ws->nfeas);
     atomicAdd(c + SAIM_CNT_PHILOX, (unsigned long long)ws->cnt[kCntPhilox]);
     atomicAdd(c + SAIM_CNT_SWEEPS, (unsigned long long)ws->cnt[kCntSweeps] + (a.T >= 2 ? (unsigned long long)a.K : 0ull));
-    atomicAdd(c + SAIM_CNT_GROUPS_SKIPPED, (unsigned long long)ws->cnt[kCntSkip]);
   }
 }
 
