@@ -209,8 +209,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     const uint32_t q_bytes = align16((uint32_t)n * QW * 128u);
     ctx->a_off = q_bytes;
     ctx->c_off = ctx->a_off + align16(NBP * 32 * 4);
-    ctx->x_off = ctx->c_off + align16(ctx->npl * 32 * 4);          // max_i |Q_ij| per spin (float)
-    ctx->blob_bytes = ctx->x_off + align16(NBP * 32 * 4);
+    ctx->blob_bytes = ctx->c_off + align16(ctx->npl * 32 * 4);
     if ((int)ctx->blob_bytes + 64 > smem_optin) {
       delete ctx;
       return fail(SAIM_ESMEM, "QKP blob of %u bytes exceeds shared memory (%d)", ctx->blob_bytes, smem_optin);
@@ -245,13 +244,6 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
       }
       int32_t *cc = reinterpret_cast<int32_t *>(B + ctx->c_off);
       for (int i = 0; i < n; ++i) cc[i] = prob->c[(size_t)s * n + i];
-      float *qm = reinterpret_cast<float *>(B + ctx->x_off);
-      for (int j = 0; j < n; ++j) {
-        long long mx = 0;
-        if (Q)
-          for (int i = 0; i < n; ++i) mx = std::max(mx, std::llabs((long long)Q[(size_t)i * n + j]));
-        qm[j] = (float)mx;
-      }
     }
     e = qkp_configure(ctx->npl, ctx->qb, ctx->smem_bytes, smem_optin, &ctx->max_wpc);
     if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "configure QKP kernel"); }

@@ -58,11 +58,6 @@ struct WarpState {
   int best_k, nfeas;
   uint32_t cnt[6];                 // flips, uniforms, fp64, uncertified, philox, sweeps evaluated
   uint32_t best_word[32];
-  // Group skip (DESIGN.md 6.1 "Quiet-group certificates"): gm = min over the group's lanes of
-  // (2x-1) z/t - e/t at its last quiet scan (field units per unit t), gd = dacc at that scan;
-  // dacc = running bound of |d(z/t)| caused by flips in this anneal.
-  float gm[8], gd[8];
-  float dacc, twok2amax;
 };
 enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps };
 
@@ -126,7 +121,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem) + lane;       // Q word (row 0, w 0) of this lane
   const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane] (NaN-padded)
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + a.c_off);
-  const float *sQmax = reinterpret_cast<const float *>(smem + a.x_off);        // max_i |Q_ij| per spin j
   unsigned char *wbase = smem + a.blob_bytes + warp * qkp_warp_smem_bytes<NPL>();
   float *phs = reinterpret_cast<float *>(wbase) + lane;                        // (2x_i - 1) phi_i, i = 32b + lane
   float *asg = reinterpret_cast<float *>(wbase) + NBP * 32 + lane;             // (2x_i - 1) A_i
@@ -151,7 +145,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     ws->k3s = 0.0f;
     ws->e0s = (float)(bstep * Hp->c_o * Hp->phi_bound * 0x1p-20);
     ws->e1s = (float)(bstep * Hp->c_p * Hp->v_bound * 0x1p-20);
-    ws->twok2amax = (float)(2.0 * bstep * Hp->c_p * (Hp->v_bound - 2.0 * Hp->r_bound)) * 1.01f;
     ws->Lam = 0;
     ws->best_f = LLONG_MAX;
     ws->best_k = -1;
@@ -172,8 +165,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   //   (stored as (2x_i - 1) phi_i), r += delta A_j.
   auto apply_flip = [&](int b, int L, float AL, float dl) {
     r2 = fmaf(dl + dl, AL, r2);
-    if (lane == 0)                                    // |d(z_i/t)| <= k1 max_i|Q_ij| + 2 k2 A_max A_j
-      ws->dacc += fmaf(ws->twok2amax, AL, ws->k1s * sQmax[32 * b + L]) * 1.01f;
     if (lane == L) {
       xm ^= (1u << b);
       phs[32 * b] = -phs[32 * b];
@@ -228,12 +219,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
-    if (lane == 0) {
-      ws->dacc = 0.0f;
-#pragma unroll
-      for (int gg = 0; gg < 8; ++gg) ws->gm[gg] = -1.0f;
-    }
-    __syncwarp();
     for (int t = t0; t < a.T; ++t) {
       const float tf = (a.T >= 2) ? (float)t : 1.0f;     // exact
       bool active = false;                            // any non-quiet lane in this sweep?
@@ -309,15 +294,13 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // spin is not certified quiet (saturated towards its current value).  With zz = (2x-1) z:
       //   zz = K1 (2x-1)phi - (2x-1)A (K2 v + K3),  v = 2r - (2x-1)A  = 2 r0 + A,
       //   quiet <=> zz > B0 + B1 |A|;  NaN padding (spins >= N) compares false -> quiet.
-      auto scan_one = [&](uint32_t &nq, float &mg, int b, int bb) {
+      auto scan_one = [&](uint32_t &nq, int b, int bb) {
         const float as = asg[32 * b];
         const float ph = phs[32 * b];
         const float v = r2 - as;
         const float tq = fmaf(K2, v, K3);
         const float zz = fmaf(K1, ph, -(as * tq));
-        const float thr = fmaf(B1, fabsf(as), B0);
-        if (zz <= thr) nq |= 1u << bb;
-        mg = fminf(mg, zz - thr);                          // NaN (no spin) is ignored by fminf
+        if (zz <= fmaf(B1, fabsf(as), B0)) nq |= 1u << bb;
       };
       // Process the non-quiet blocks of group g in order (exactly); after a flip the later
       // blocks' speculation is stale, so they are rescanned.
@@ -332,37 +315,21 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           }
           if (bstart >= 4) return;
           uint32_t nq = 0;
-          float mg = INFINITY;
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb)
-            if (bb >= bstart) scan_one(nq, mg, 4 * g + bb, bb);
+            if (bb >= bstart) scan_one(nq, 4 * g + bb, bb);
           m = __reduce_or_sync(kFull, nq);
           if (!m) return;
         }
       };
 
-      const float inv_t = 1.0f / tf;
       for (g = 0; g < NG; ++g) {
-        // certified-quiet group: t (gm - (dacc - gd)) > ln(2^24-1) (1% and 2^-20 safety margins)
-        if (tf * (ws->gm[g] - 1.01f * (ws->dacc - ws->gd[g])) * (1.0f - 0x1p-20f) > kSatThr) continue;
         have_u = false;
         uint32_t nq = 0;
-        float mg = INFINITY;
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) scan_one(nq, mg, 4 * g + bb, bb);
+        for (int bb = 0; bb < 4; ++bb) scan_one(nq, 4 * g + bb, bb);
         const uint32_t m = __reduce_or_sync(kFull, nq);
-        if (m) {
-          handle_group(m);
-          if (lane == 0) ws->gm[g] = -1.0f;               // margins unknown after processing
-        } else {
-          // every lane quiet: record the group's minimum margin (non-negative here)
-          const uint32_t mb = __reduce_min_sync(kFull, __float_as_uint(fmaxf(mg, 0.0f)));
-          if (lane == 0) {
-            ws->gm[g] = (__uint_as_float(mb) + kSatThr) * inv_t;
-            ws->gd[g] = ws->dacc;
-          }
-        }
-        __syncwarp();
+        if (m) handle_group(m);
       }
       cnt_add(ws, kCntSweeps, 1);
       // Frozen anneal: a sweep in which every spin was certified
