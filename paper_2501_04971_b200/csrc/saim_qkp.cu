@@ -244,6 +244,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         bool have_l = false;                              // logit of this lane's u, drawn once per visit
         float l = 0.0f, el = 0.0f;
         uint32_t w = 0;
+        uint32_t drew = 0;                                // lanes that needed their uniform in this visit
         int lo = 0;                                       // lanes in [lo, hi) are still pending
         for (;;) {
           const float phib = -sg * phs[32 * b];           // phi_i
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
               el = kLogitAbs + kLogitRel * fabsf(l);
               have_l = true;
             }
-            cnt_add(ws, kCntUnif, __popc(need));
+            drew |= need;
             if (mine && !sat) {
               const float d = z - l;
               if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           lo = L + 1;
           if (lo >= hi) break;
         }
+        if (drew) cnt_add(ws, kCntUnif, __popc(drew));
         return flipped;
       };
 
