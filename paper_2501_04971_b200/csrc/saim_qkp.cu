@@ -58,6 +58,9 @@ struct WarpState {
   int best_k, nfeas;
   uint32_t cnt[6];                 // flips, uniforms, fp64, uncertified, philox, sweeps evaluated
   uint32_t best_word[32];
+  uint2 key;                        // Philox key (lo32 seed, hi32 seed)
+  uint32_t srho;                    // (s << 20) | rho
+  uint32_t uw[4][32];               // lazily drawn words of the current group, per lane
 };
 enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps };
 
@@ -157,8 +160,11 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
-  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
-  const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)(a.rep0 + ridx);
+  if (lane == 0) {
+    ws->key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+    ws->srho = ((uint32_t)s << 20) | (uint32_t)(a.rep0 + ridx);
+  }
+  __syncwarp();
 
   // Flip of spin j = 32b + L by delta = dl (+1/-1): Eq. 9 in incremental form.
   //   own lane: x_j, and the signs of its (2x-1) phi, (2x-1) A;  all lanes: phi_i -= delta Q_ij
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // ---- sweep t = 0: beta_0 = 0, x_i = [u < 1/2] (state-independent; R3, R5) ----
       t0 = 1;
       for (int g = 0; g < NG; ++g) {
-        const uint4 uw = philox_group(key, g, lane, 0, k, srho);
+        const uint4 uw = philox_group(ws->key, g, lane, 0, k, ws->srho);
         cnt_add(ws, kCntPhilox, 32);
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) {
@@ -228,8 +234,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // bounds |z_f32 - z| for every reachable state (phi_bound, v_bound; 4x margin over 3*2^-24).
       const float B0 = fmaf(tf, ws->e0s, kSatThr), B1 = tf * ws->e1s;
       int g = 0;                                          // current 128-spin group (4 blocks)
-      uint4 uw = make_uint4(0, 0, 0, 0);                  // group g's uniforms, drawn lazily
-      bool have_u = false;
+      bool have_u = false;                                // group g's words drawn (ws->uw)?
 
       // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
       // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
@@ -258,11 +263,12 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           if (need) {
             if (!have_l) {
               if (!have_u) {
-                uw = philox_group_lazy(key, g, lane, t, k, srho);
+                const uint4 u4 = philox_group_lazy(ws->key, g, lane, t, k, ws->srho);
+                ws->uw[0][lane] = u4.x; ws->uw[1][lane] = u4.y; ws->uw[2][lane] = u4.z; ws->uw[3][lane] = u4.w;
                 have_u = true;
                 cnt_add(ws, kCntPhilox, 32);
               }
-              w = sel4(uw, bb);
+              w = ws->uw[bb][lane];
               l = logit_f32(w);
               el = kLogitAbs + kLogitRel * fabsf(l);
               have_l = true;
