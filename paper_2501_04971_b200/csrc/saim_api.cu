@@ -138,6 +138,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     long long rmax = 0;
     for (int k = 0; k < M; ++k) {
       if (b[k] < 1) { delete ctx; return fail(SAIM_EINVAL, "b[%d][%d] must be >= 1", s, k); }
+      if (b[k] >= (1LL << 30)) { delete ctx; return fail(SAIM_ERANGE, "b[%d][%d] >= 2^30", s, k); }
       sc = std::max(sc, (long long)b[k]);
       long long load = 0;
       for (int j = 0; j < n; ++j) {
@@ -246,6 +247,10 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
       for (int i = 0; i < n; ++i) cc[i] = prob->c[(size_t)s * n + i];
     }
     e = qkp_configure(ctx->npl, ctx->qb, ctx->smem_bytes, smem_optin, &ctx->max_wpc);
+    if (e == cudaErrorInvalidConfiguration) {
+      delete ctx;
+      return fail(SAIM_ESMEM, "QKP layout (%u bytes) leaves no room for one warp's state in shared memory", ctx->blob_bytes);
+    }
     if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "configure QKP kernel"); }
     ctx->lanes = 32;
   } else if (!prob->Q) {

@@ -252,3 +252,44 @@ def test_mkp_parity_config4_sampled(P):
     g = run_both(P, cfg.instances[:8], cfg.P[:8], cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=4, T=cfg.T,
                  reps=[0, 255])
     assert g["info"]["kernel"] == 2
+
+
+# ---------------------------------------------------------------------------------------------
+# Maximum sizes and degenerate problems
+
+def test_qkp_largest_resident_instance(P):
+    """n = 420 items (int8 Q, 4 words per lane-row: ~212 KB of shared memory, one warp per CTA)."""
+    p = _qkp(420, 0.5, 11)
+    g = run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=14, R=3, K=2, T=6)
+    assert g["info"]["smem_bytes"] > 200_000
+
+
+def test_qkp_too_large_is_esmem(P):
+    p = _qkp(470, 0.5, 12)
+    with pytest.raises(P.SaimError) as ei:
+        P.Solver(p.Q, p.c, p.A, p.b, 10.0, 20.0, 10.0)
+    assert ei.value.code == P.SAIM_ESMEM
+
+
+def test_mkp_largest_constraint_count(P):
+    """M = 32 constraints (the MKP kernel's maximum) with n = 300 items."""
+    p = _mkp(300, 32, 0.5, 3)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=15, R=33, K=2, T=4)
+
+
+def test_degenerate_problems(P):
+    # zero objective: only the penalty and Lagrange terms act
+    p = _qkp(40, 0.5, 13)
+    p.Q[:] = 0
+    p.c[:] = 0
+    run_both(P, [p], [2.0], 20.0, 10.0, seed=16, R=8, K=4, T=20)
+    # P = 0 (no penalty): the Lagrange term alone shapes L
+    p = _qkp(40, 0.5, 14)
+    run_both(P, [p], [0.0], 20.0, 10.0, seed=17, R=8, K=4, T=20)
+    # huge beta_max: everything saturates after the first sweeps (deterministic descent)
+    run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 1e6, seed=18, R=8, K=4, T=20)
+    # MKP with a row of zero weights (its slack bits still exist)
+    m = _mkp(30, 3, 0.5, 4)
+    m.A[1, :] = 0
+    m.b[1] = 7
+    run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=19, R=32, K=3, T=20)
