@@ -286,8 +286,9 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
         ic[4 * i + 0] = cphi;
         ic[4 * i + 1] = cpa;
         ic[4 * i + 2] = (float)a1;
-        // E0_i = 2 (MM+6) 2^-24 (|c_o c_i| + c_p a_i), DESIGN.md 6.2 (factor 2: margin)
-        ic[4 * i + 3] = (float)(2.0 * (MM + 6) * 0x1p-24 * (fabs((double)cphi) + (double)cpa));
+        // E0_i = (2 (MM+6) 2^-24 + 1.01 2^-22) (|c_o c_i| + c_p a_i), DESIGN.md 6.2 (factor 2:
+        // margin; the 2^-22 term bounds the final rounding of z through |z|'s static bound)
+        ic[4 * i + 3] = (float)((2.0 * (MM + 6) * 0x1p-24 + 1.01 * 0x1p-22) * (fabs((double)cphi) + (double)cpa));
         cc[i] = ci;
       }
       for (int k = 0; k < M; ++k) {

@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
     }
     // |z_f32 - z| <= beta (E1 |A_i|_1 + E0_i) + 2^-23 |z|, E = (MM+8) 2^-24 (...):
     // the lookahead's band value adds |A_i . A_{i-1}| <= |A_i|_1 max A; factor 2: safety margin.
-    const float E1 =
-        (float)((MM + 8) * 0x1p-24 * (2.0 * c_p * ((double)rbound + (double)amax) + (double)cLmax)) * 2.0f;
+    // + 2^-22 |z| folded in with |z| <= beta (|c_o c_i| + c_p a_i + |A_i|_1 (2 c_p r_max + max|c_l Lambda|))
+    const double Wk = 2.0 * c_p * ((double)rbound + (double)amax) + (double)cLmax;
+    const float E1 = (float)((MM + 8) * 0x1p-24 * Wk * 2.0 + 0x1p-22 * Wk * 1.01);
 
     for (int t = 0; t < a.T; ++t) {
       const bool bz = (a.T >= 2) && (t == 0);          // beta_0 = 0: x_i = [u < 1/2]
@@ -148,13 +149,16 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // (exact sign), evaluated branch-free; only the rare fp64 re-evaluation (slow(): returns
       // x | uncertified << 1) sits behind a warp vote.
       auto decide = [&](float z, float e, float l, auto slow) -> int {
-        const bool sat = fabsf(z) - e > kSatThr;
+        // e bounds |z_f32 - z| for every reachable state and does not depend on z, so both
+        // thresholds are ready before z: the dependency chain is z -> d -> compare.
+        const float satT = e + kSatThr;
+        const float certT = (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f;
         const float d = z - l;
-        const bool cert = fabsf(d) > (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f;
+        const bool sat = fabsf(z) > satT;
         int nx = sat ? (z > 0.0f) : (d > 0.0f);
         if (bz) nx = (int)(__float_as_uint(l) >> 31);     // beta_0 = 0: u < 1/2 (sign bit, -0 included)
         c_unif += (!bz && !sat) ? 1u : 0u;
-        const bool need = !bz && !sat && !cert;
+        const bool need = !bz && !sat && !(fabsf(d) > certT);
         if (__any_sync(kFull, need)) {
           if (need) {
             ++c_fp64;
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           const float sg = xb ? -1.0f : 1.0f;             // 1 - 2 x_i
           const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
           const float z = bf * F;
-          const float e = bf * fmaf(E1, ic.z, ic.w) + fabsf(z) * 0x1p-22f;
+          const float e = bf * fmaf(E1, ic.z, ic.w);
           const int nx = decide(z, e, l, [&]() -> int {
             const uint32_t wd = word_of(key, i, t, k, srho);
             double drd = 0.0, dld = 0.0, a2 = 0.0;
@@ -254,8 +258,9 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           const float inner = fmaf(twocp, r[m], cL[m]);
           const float F = -(A * inner) - (cpf * A) * A * sg;
           const float z = bf * F;
-          const float e = bf * 8.0f * 0x1p-24f * fmaf(A, fabsf(twocp * r[m]) + fabsf(cL[m]), cpf * A * A) +
-                          fabsf(z) * 0x1p-22f;
+          // |z_f32 - z| <= beta (8 2^-24 + 1.01 2^-22) (A (|2 c_p r_m| + |c_l Lambda_m|) + c_p A^2)
+          const float e = bf * (8.0f * 0x1p-24f + 1.01f * 0x1p-22f) *
+                          fmaf(A, fabsf(twocp * r[m]) + fabsf(cL[m]), cpf * A * A);
           const int nx = decide(z, e, l, [&]() -> int {
             const uint32_t w = word_of(key, i, t, k, srho);
             const double Ad = (double)A;
