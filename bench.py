@@ -45,6 +45,21 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def ncu_traffic_bytes():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the SAIM kernel per launch, from the committed
+    ncu --set full capture of the same workload (profiles/r01/qkp_config2_K200_raw_selected.csv)."""
+    p = os.path.join(ROOT, "profiles", "r01", "qkp_config2_K200_raw_selected.csv")
+    if not os.path.exists(p):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for ln in open(p).read().splitlines()[1:]:
+        name, unit, val = ln.split(",", 2)
+        if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(val) * scale.get(unit, 1)
+    return tot
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -319,7 +334,8 @@ def main():
             "samples_per_s": samples_per_s,
             "gpu_launches": 2 * args.steps,
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-                         "frac": achieved / peak_ops, "traffic": None,
+                         "frac": achieved / peak_ops, "traffic": ncu_traffic_bytes(),
+                         "traffic_unit": "DRAM bytes per launch (ncu capture in profiles/r01; the path is on-chip)",
                          "ops_per_launch": ops, "ops_model": f"{OPS_DECISION}*evaluated decisions + {OPS_UNIFORM}*uniforms + "
                                                             f"{OPS_FLIP_PER_ITEM}*n*flips (lane-ops)",
                          "peak_basis": f"{sm_count} SMs x {LANES_PER_SM_CLK} lanes/clk x {sm_mhz:.0f} MHz "
