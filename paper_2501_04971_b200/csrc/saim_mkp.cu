@@ -53,7 +53,9 @@ struct MkpCfg {
 
 }  // namespace
 
-template <int MM>
+// MM: padded constraint count (layout); MA <= MM: rows the arithmetic loops cover (= M for the
+// instantiated exact sizes, else MM with zero-padded rows).
+template <int MM, int MA>
 __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const RunArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t mbar;
@@ -178,12 +180,13 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
         float dr0 = 0.f, dr1 = 0.f, dl0 = 0.f, dl1 = 0.f;
 #pragma unroll
-        for (int m4 = 0; m4 < MM / 4; ++m4) {
+        for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
           const float4 av = Ac[m4];
-          dr0 = fmaf(av.x, r[4 * m4 + 0], dr0); dr1 = fmaf(av.y, r[4 * m4 + 1], dr1);
-          dr0 = fmaf(av.z, r[4 * m4 + 2], dr0); dr1 = fmaf(av.w, r[4 * m4 + 3], dr1);
-          dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1);
-          dl0 = fmaf(av.z, cL[4 * m4 + 2], dl0); dl1 = fmaf(av.w, cL[4 * m4 + 3], dl1);
+          dr0 = fmaf(av.x, r[4 * m4 + 0], dr0);
+          dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0);
+          if (4 * m4 + 1 < MA) { dr1 = fmaf(av.y, r[4 * m4 + 1], dr1); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1); }
+          if (4 * m4 + 2 < MA) { dr0 = fmaf(av.z, r[4 * m4 + 2], dr0); dl0 = fmaf(av.z, cL[4 * m4 + 2], dl0); }
+          if (4 * m4 + 3 < MA) { dr1 = fmaf(av.w, r[4 * m4 + 3], dr1); dl1 = fmaf(av.w, cL[4 * m4 + 3], dl1); }
         }
         pr = dr0 + dr1;
         dlv = dl0 + dl1;
@@ -228,12 +231,12 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           const float dl = (float)(nx - xb);              // delta in {-1, 0, +1}; fma(0, A, r) == r
           const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
 #pragma unroll
-          for (int m4 = 0; m4 < MM / 4; ++m4) {
+          for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
             const float4 av = Ac[m4];
             r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
-            r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
-            r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
-            r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
+            if (4 * m4 + 1 < MA) r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
+            if (4 * m4 + 2 < MA) r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
+            if (4 * m4 + 3 < MA) r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
           }
           xcur ^= (uint32_t)(nx != xb) << ii;
           c_flips += (nx != xb) ? 1u : 0u;
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       int i = n;
       xcur = xw[32 * (n >> 5)];                            // word holding spin n (stored by the item loop)
 #pragma unroll
-      for (int m = 0; m < MM; ++m) {
+      for (int m = 0; m < MA; ++m) {
         const int qm = (m < M) ? sQ[m] : 0;
         for (int q = 0; q < qm; ++q, ++i) {
           if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
@@ -385,15 +388,19 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
 
 // ---------------------------------------------------------------------------------------------
 typedef void (*mkp_kernel_t)(const RunArgs);
+// (MM, M) -> kernel: exact arithmetic widths for the paper's MKP sizes (M = 5, 10, 30).
 
 static int mm_for(int M) { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : -1))); }
 
-static mkp_kernel_t mkp_kernel_for(int MM) {
+static mkp_kernel_t mkp_kernel_for(int MM, int M) {
+  if (MM == 8 && M == 5) return saim_mkp_kernel<8, 5>;
+  if (MM == 16 && M == 10) return saim_mkp_kernel<16, 10>;
+  if (MM == 32 && M == 30) return saim_mkp_kernel<32, 30>;
   switch (MM) {
-    case 4: return saim_mkp_kernel<4>;
-    case 8: return saim_mkp_kernel<8>;
-    case 16: return saim_mkp_kernel<16>;
-    case 32: return saim_mkp_kernel<32>;
+    case 4: return saim_mkp_kernel<4, 4>;
+    case 8: return saim_mkp_kernel<8, 8>;
+    case 16: return saim_mkp_kernel<16, 16>;
+    case 32: return saim_mkp_kernel<32, 32>;
     default: return nullptr;
   }
 }
@@ -404,7 +411,7 @@ int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blo
              int *max_wpc) {
   const int MM = mm_for(M);
   if (MM < 0) return -1;
-  mkp_kernel_t k = mkp_kernel_for(MM);
+  mkp_kernel_t k = mkp_kernel_for(MM, M);
   cudaFuncAttributes attr;
   if (cudaFuncGetAttributes(&attr, k) != cudaSuccess) return -1;
   const MkpLayout L = mkp_layout(n, MM);
@@ -424,7 +431,7 @@ int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blo
 }
 
 cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st) {
-  mkp_kernel_t k = mkp_kernel_for(MM);
+  mkp_kernel_t k = mkp_kernel_for(MM, a.M);
   if (!k) return cudaErrorInvalidValue;
   const int warps_per_inst = (a.R + 31) / 32;
   dim3 grid((warps_per_inst + wpc - 1) / wpc, n_inst);

@@ -223,7 +223,7 @@ def _mkp(n, m, t, seed):
     return si.mkp(n, m, t, [88, n, m, seed])
 
 
-@pytest.mark.parametrize("n,m", [(7, 2), (30, 3), (33, 5), (64, 8), (40, 9), (20, 16), (25, 30)])
+@pytest.mark.parametrize("n,m", [(7, 2), (30, 3), (33, 5), (64, 8), (40, 9), (26, 10), (20, 16), (25, 30), (22, 32)])
 def test_mkp_parity_small(P, n, m):
     """Small MKP instances across the constraint-count buckets (MM = 4, 8, 16, 32) with ragged N."""
     p = _mkp(n, m, 0.5, 1)
