@@ -42,7 +42,7 @@ extern "C" {
 #define SAIM_CNT_DECISIONS 0     /* attempted p-bit updates = n_inst*R*K*T*N */
 #define SAIM_CNT_FLIPS 1         /* decisions that changed x_i (identical to the oracle's count) */
 #define SAIM_CNT_SWEEPS 2        /* sweeps actually evaluated (the rest were certified frozen, see flags) */
-#define SAIM_CNT_UNIFORMS 3      /* decisions for which the uniform u had to be drawn (unsaturated) */
+#define SAIM_CNT_UNIFORMS 3      /* decisions the kernel could not settle without u (not certified saturated) */
 #define SAIM_CNT_FP64 4          /* decisions re-evaluated on the fp64 slow path */
 #define SAIM_CNT_UNCERTIFIED 5   /* decisions not certified even in fp64 (expected 0) */
 #define SAIM_CNT_FEASIBLE 6      /* feasible samples x_k */
@@ -74,6 +74,13 @@ typedef struct {
  * constant and beta_t only grows, so all later sweeps of that anneal provably change nothing
  * (DESIGN.md "Exact early exit").  Results are bit-identical either way. */
 #define SAIM_FLAG_NO_FREEZE_EXIT 1
+/* Kernel selection for linear objectives with M >= 2 constraints (MKP).  Default: the
+ * outcome-tree kernel with L = 2 lanes per replica for M <= 8, the lane-per-replica lockstep
+ * kernel for M > 8 (the faster one on B200).  These flags force the lockstep kernel or the
+ * outcome tree with a given L.  All produce identical results. */
+#define SAIM_FLAG_MKP_LOCKSTEP 2
+#define SAIM_FLAG_MKP_L2 4
+#define SAIM_FLAG_MKP_L4 8
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),

@@ -20,6 +20,9 @@ LIB_PATH = os.path.join(_HERE, "libsaim.so")
 SAIM_OK, SAIM_EINVAL, SAIM_ERANGE, SAIM_ESMEM, SAIM_ECUDA, SAIM_EUNSUPPORTED, SAIM_ENOMEM = 0, -1, -2, -3, -4, -5, -6
 COUNTER_NAMES = ["decisions", "flips", "sweeps", "uniforms", "fp64", "uncertified", "feasible", "philox"]
 FLAG_NO_FREEZE_EXIT = 1
+FLAG_MKP_LOCKSTEP = 2      # MKP: lane-per-replica kernel instead of the outcome tree
+FLAG_MKP_L2 = 4            # MKP: outcome tree with 2 lanes per replica
+FLAG_MKP_L4 = 8            # MKP: outcome tree with 4 lanes per replica
 EXPORTS = ["saim_create", "saim_run", "saim_get_info", "saim_get_instance", "saim_destroy",
            "saim_last_error", "saim_selftest"]
 

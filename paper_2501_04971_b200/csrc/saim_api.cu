@@ -26,6 +26,8 @@ cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, i
 int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
              int *max_wpc);
 cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
+int mkpt_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, int L, uint32_t *per_warp, int *max_wpc);
+cudaError_t mkpt_launch(const RunArgs &a, int n_inst, int MM, int L, int wpc, uint32_t per_warp, cudaStream_t st);
 int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 }  // namespace saim
 
@@ -52,7 +54,7 @@ struct saim_ctx {
   int n_inst = 0, n = 0, M = 0;
   int kernel = 0;       // 1 = QKP, 2 = MKP
   int npl = 0, qb = 0;  // QKP
-  int lanes = 32;       // lanes per replica (QKP: 32; MKP: 1, lockstep)
+  int lanes = 32;       // lanes per replica (QKP: 32; MKP: 1 lockstep, L = 2 or 4 outcome tree)
   int mm = 0;           // MKP padded constraint count
   uint32_t per_warp = 0;
   int N_max = 0, n_slack_max = 0;
@@ -95,6 +97,9 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     return fail(SAIM_EINVAL, "missing c/A/b/P array");
   if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
   if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
+  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) ||
+      __builtin_popcount(par->flags & (SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) > 1)
+    return fail(SAIM_EINVAL, "unknown or conflicting flags 0x%x", par->flags);
 
   if (M > 1 && prob->Q)
     return fail(SAIM_EUNSUPPORTED, "quadratic objective with M = %d > 1 constraints has no kernel", M);
@@ -264,6 +269,24 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     const int MM = ctx->mm;
     const MkpLayout L = mkp_layout(n, MM);
     ctx->smem_bytes = (int)(L.bytes + ctx->per_warp);
+    // Default (measured on B200): outcome tree with L = 2 for M <= 8 (config 3:
+    // 1.15x the lockstep kernel), lockstep for larger M (config 4: 1.7x the tree).
+    const bool tree = (ctx->flags & (SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) ||
+                      (!(ctx->flags & SAIM_FLAG_MKP_LOCKSTEP) && M <= 8);
+    if (tree) {   // outcome-tree kernel (saim_mkp_tree.cu)
+      const int lanes = (ctx->flags & SAIM_FLAG_MKP_L4) ? 4 : 2;
+      uint32_t pw = 0;
+      int wpc = 0;
+      if (mkpt_plan(M, ctx->N_max, smem_optin, MM, L.bytes, lanes, &pw, &wpc) == 0) {
+        ctx->lanes = lanes;
+        ctx->per_warp = pw;
+        ctx->max_wpc = wpc;
+        ctx->smem_bytes = (int)(L.bytes + pw);
+      } else if (ctx->flags & (SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) {
+        delete ctx;
+        return fail(SAIM_ESMEM, "MKP outcome-tree kernel (L=%d) does not fit shared memory", lanes);
+      }
+    }
     blob.assign((size_t)S * ctx->blob_bytes, 0);
     for (int s = 0; s < S; ++s) {
       unsigned char *B = blob.data() + (size_t)s * ctx->blob_bytes;
@@ -296,13 +319,14 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
         qrow[k] = ctx->q[s][k];
       }
       float *band = reinterpret_cast<float *>(B + L.band);
-      band[0] = 0.0f;
-      for (int i = 1; i < n; ++i) {
-        double g = 0.0;
-        for (int k = 0; k < M; ++k)
-          g += (double)prob->A[((size_t)s * M + k) * n + i] * (double)prob->A[((size_t)s * M + k) * n + i - 1];
-        band[i] = (float)g;
-      }
+      const uint32_t bs = mkp_band_stride(n);
+      for (int d = 1; d <= 3; ++d)
+        for (int i = d; i < n; ++i) {
+          double g = 0.0;
+          for (int k = 0; k < M; ++k)
+            g += (double)prob->A[((size_t)s * M + k) * n + i] * (double)prob->A[((size_t)s * M + k) * n + i - d];
+          band[(d - 1) * bs + i] = (float)g;
+        }
     }
   } else {
     delete ctx;
@@ -356,11 +380,19 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
     e = qkp_launch(ctx->npl, ctx->qb, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
-  } else {
+  } else if (ctx->lanes == 1) {
     const long long warps = (long long)((R + 31) / 32) * ctx->n_inst;   // 32 replicas per warp (lockstep)
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
     e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st);
+  } else {
+    // one CTA per SM: spread each instance's warps over floor(SMs / n_inst) CTAs
+    const int G = 32 / ctx->lanes;
+    const int warps_inst = (R + G - 1) / G;
+    const int ctas_inst = std::max(1, ctx->sm_count / ctx->n_inst);
+    int wpc = (warps_inst + ctas_inst - 1) / ctas_inst;
+    wpc = std::max(1, std::min(wpc, ctx->max_wpc));
+    e = mkpt_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SAIM_OK;

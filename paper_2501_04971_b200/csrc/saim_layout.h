@@ -49,8 +49,9 @@ inline __host__ __device__ uint32_t align16u(uint32_t v) { return (v + 15u) & ~1
 //   cint   int32 [n]       c_i (exact objective for the readout)
 //   brow   int64 [MM]      b_m
 //   qrow   int32 [MM]      slack bit count q_m (0 for padded rows)
-//   band   float [n]       G_i = A_{.i} . A_{.i-1} (adjacent item columns; G_0 = 0) -- the O(n)
-//                          band used by the one-spin lookahead, not the dense A^T A
+//   band   float [3][n+1]  G_d[i] = A_{.i} . A_{.i-d}, d = 1..3 (0 where i < d): the O(3n) band of
+//                          nearby item-column products used by the lookahead / outcome trees --
+//                          not the dense A^T A
 struct MkpLayout {
   uint32_t acol, iconst, cint, brow, qrow, band, bytes;
 };
@@ -62,14 +63,22 @@ inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
   L.cint = o;   o += align16u((uint32_t)n * 4u);
   L.brow = o;   o += (uint32_t)MM * 8u;
   L.qrow = o;   o += align16u((uint32_t)MM * 4u);
-  L.band = o;   o += align16u((uint32_t)(n + 1) * 4u);
+  L.band = o;   o += 3u * align16u((uint32_t)(n + 1) * 4u);
   L.bytes = o;
   return L;
 }
-// Per-warp MKP shared memory: x bits [WN][32 lanes], logits of the current 128-spin group
-// [128][32] floats, Lambda [MM][32] int64.
+inline __host__ __device__ uint32_t mkp_band_stride(int n) { return align16u((uint32_t)(n + 1) * 4u) / 4u; }
+// Per-warp MKP shared memory (lockstep kernel): x bits [WN][32 lanes], logits of the current
+// 128-spin group [128][32] floats, Lambda [MM][32] int64.
 inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM) {
   return align16u((uint32_t)WN * 128u) + 128u * 128u + (uint32_t)MM * 256u;
+}
+// Per-warp shared memory of the outcome-tree kernel with L lanes per replica (G = 32/L replica
+// groups): x bits [WN][G] words, logits of the current 128-spin group [128][G] floats, Lambda
+// [MM][G] int64.
+inline __host__ __device__ uint32_t mkpt_warp_bytes(int WN, int L, int MM) {
+  const uint32_t G = 32u / (uint32_t)L;
+  return align16u((uint32_t)WN * G * 4u) + 128u * G * 4u + (uint32_t)MM * G * 8u;
 }
 
 struct RunArgs {

@@ -66,9 +66,9 @@ def compare(g, o, s, reps, N, K, M):
             assert np.array_equal(g["final_lam"][s, reps], o["final_lam"])
 
 
-def run_both(P, probs, Pens, eta, beta_max, seed, R, K, T, reps=None, rep0=0):
+def run_both(P, probs, Pens, eta, beta_max, seed, R, K, T, reps=None, rep0=0, flags=0):
     Q, c, A, b = si.stack(probs)
-    g = gpu_run(P, Q, c, A, b, Pens, eta, beta_max, seed, R, K, T, rep0=rep0)
+    g = gpu_run(P, Q, c, A, b, Pens, eta, beta_max, seed, R, K, T, rep0=rep0, flags=flags)
     assert g["counters"]["uncertified"] == 0
     flips = 0
     for s, pr in enumerate(probs):
@@ -223,26 +223,53 @@ def _mkp(n, m, t, seed):
     return si.mkp(n, m, t, [88, n, m, seed])
 
 
+# MKP kernel variants: default (outcome tree, L by M), lockstep, outcome tree with L = 2 and 4
+MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("tree_L2", 4), ("tree_L4", 8)]
+MKP_LANES = {0: None, 2: 1, 4: 2, 8: 4}
+
+
+@pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
 @pytest.mark.parametrize("n,m", [(7, 2), (30, 3), (33, 5), (64, 8), (40, 9), (26, 10), (20, 16), (25, 30), (22, 32)])
-def test_mkp_parity_small(P, n, m):
-    """Small MKP instances across the constraint-count buckets (MM = 4, 8, 16, 32) with ragged N."""
+def test_mkp_parity_small(P, n, m, variant):
+    """Small MKP instances across the constraint-count buckets (MM = 4, 8, 16, 32) with ragged N,
+    for every MKP kernel (R = 40 leaves a partial replica group / warp)."""
     p = _mkp(n, m, 0.5, 1)
-    g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=40, K=4, T=30)
+    g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=40, K=4, T=30, flags=variant)
     assert g["info"]["kernel"] == 2
+    want = MKP_LANES[variant] or (2 if m <= 8 else 1)
+    assert g["info"]["lanes_per_replica"] == want
 
 
-def test_mkp_parity_tiny_capacities(P):
+@pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
+def test_mkp_parity_tiny_capacities(P, variant):
     p = _mkp(12, 3, 0.1, 2)
     p.b[:] = [1, 2, 3]
-    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=5, T=25)
-    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=3, T=1)      # fixed beta
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=5, T=25, flags=variant)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=3, T=1, flags=variant)  # fixed beta
 
 
-def test_mkp_parity_config3_sampled(P):
+def test_mkp_kernels_agree_on_counters(P):
+    """All MKP kernels make the same decisions, so every output and the data-determined counters
+    (flips, feasible samples, Philox calls) agree exactly.  ('uniforms' is not compared: whether a
+    spin within a rounding margin of saturation counts as having drawn u depends on each kernel's
+    error bound; the decision itself is certified either way.)"""
+    p = _mkp(100, 5, 0.5, 21)
+    Q, c, A, b = si.stack([p])
+    runs = [gpu_run(P, Q, c, A, b, [si.paper_P(p, 5.0)], 0.05, 50.0, 3, 70, 6, 60, flags=v) for _, v in MKP_VARIANTS]
+    for r in runs[1:]:
+        for k in ["tr_x", "tr_f", "tr_feas", "tr_r", "tr_lam", "best_f", "best_k", "best_x", "n_feasible",
+                  "final_x", "final_lam", "inst_best"]:
+            assert np.array_equal(runs[0][k], r[k]), k
+        for k in ["decisions", "flips", "sweeps", "feasible", "philox", "uncertified"]:
+            assert runs[0]["counters"][k] == r["counters"][k], k
+
+
+@pytest.mark.parametrize("variant", [0, 2], ids=["default", "lockstep"])
+def test_mkp_parity_config3_sampled(P, variant):
     """Config 3 (three tightness variants in one launch) at full size; sampled replicas."""
     cfg = si.config_instances(3)
     run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
-             reps=[0, 2047])
+             reps=[0, 2047], flags=variant)
 
 
 def test_mkp_parity_config4_sampled(P):
@@ -271,10 +298,11 @@ def test_qkp_too_large_is_esmem(P):
     assert ei.value.code == P.SAIM_ESMEM
 
 
-def test_mkp_largest_constraint_count(P):
-    """M = 32 constraints (the MKP kernel's maximum) with n = 300 items."""
+@pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
+def test_mkp_largest_constraint_count(P, variant):
+    """M = 32 constraints (the MKP kernels' maximum) with n = 300 items."""
     p = _mkp(300, 32, 0.5, 3)
-    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=15, R=33, K=2, T=4)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=15, R=33, K=2, T=4, flags=variant)
 
 
 def test_degenerate_problems(P):
@@ -292,4 +320,5 @@ def test_degenerate_problems(P):
     m = _mkp(30, 3, 0.5, 4)
     m.A[1, :] = 0
     m.b[1] = 7
-    run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=19, R=32, K=3, T=20)
+    for v in (0, 2, 4, 8):
+        run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=19, R=32, K=3, T=20, flags=v)

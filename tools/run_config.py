@@ -17,10 +17,11 @@ def main():
     ap.add_argument("--T", type=int, default=None)
     ap.add_argument("--R", type=int, default=None)
     ap.add_argument("--reps", type=int, default=1)
+    ap.add_argument("--flags", type=int, default=0)
     a = ap.parse_args()
     import torch
     cfg = si.config_instances(a.config)
-    sol = P.Solver.from_config(cfg)
+    sol = P.Solver.from_config(cfg, flags=a.flags)
     R, K, T = a.R or cfg.R, a.K or cfg.K, a.T or cfg.T
     out = sol.alloc_outputs(R, K)
     for i in range(a.reps):
@@ -30,7 +31,7 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         c = P.counters_dict(out["counters"])
-        print(f"config {a.config} R={R} K={K} T={T}: {dt*1e3:.2f} ms, {c['decisions']/dt:.3e} updates/s, {c}")
+        print(f"config {a.config} flags={a.flags} lanes={sol.info['lanes_per_replica']} R={R} K={K} T={T}: {dt*1e3:.2f} ms, {c['decisions']/dt:.3e} updates/s, {c}")
     sol.close()
 
 
