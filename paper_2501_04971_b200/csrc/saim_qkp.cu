@@ -49,6 +49,7 @@ __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
 // Per-warp cold state in shared memory (kept out of the register file: the hot loop runs at
 // 28 warps/SM, i.e. <= 72 registers per thread).
 struct WarpState {
+  uint32_t gq[8];                  // group g was certified quiet when the flip count was gq[g] - 1
   float k1s, k2s, k3s;             // per unit t: K1 = t*bstep*c_o, K2 = t*bstep*c_p, K3 = t*bstep*c_l*Lambda
   float e0s, e1s;                  // scan error bound per unit t: e(A) = t*(e0s + e1s*A)
   float pad;
@@ -225,6 +226,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
+    if (lane < 8) ws->gq[lane] = 0u;                    // new Lambda_k: every group is scanned again
+    __syncwarp();
     for (int t = t0; t < a.T; ++t) {
       const float tf = (a.T >= 2) ? (float)t : 1.0f;     // exact
       bool active = false;                            // any non-quiet lane in this sweep?
@@ -332,11 +335,20 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       };
 
       for (g = 0; g < NG; ++g) {
+        // Quiet carry-over: a group whose every spin was certified
+        // saturated towards its value stays so while no spin flips -- the fields are unchanged and
+        // beta_t only grows, so (2x-1) z only moves away from the threshold.
+        if (__all_sync(kFull, ws->gq[g] == ws->cnt[kCntFlips] + 1u)) continue;   // (vote: provably uniform)
         have_u = false;
         uint32_t nq = 0;
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb) scan_one(nq, 4 * g + bb, bb);
         const uint32_t m = __reduce_or_sync(kFull, nq);
+#ifdef SAIM_STATS
+        cnt_add(ws, kCntUncert, 1);
+#endif
+        // (re-read rather than kept live across the scan: registers are the limit at 28 warps/SM)
+        if (lane == 0) ws->gq[g] = m ? 0u : *reinterpret_cast<volatile uint32_t *>(&ws->cnt[kCntFlips]) + 1u;
         if (m) handle_group(m);
       }
       cnt_add(ws, kCntSweeps, 1);
