@@ -369,6 +369,10 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
   a.Wn = (ctx->n + 31) / 32; a.WN = (ctx->N_max + 31) / 32;
   a.R = R; a.rep0 = rep0; a.K = K; a.T = T;
   a.seed = seed; a.beta_max = ctx->beta_max;
+  for (int r = 0; r < 10; ++r) {
+    a.ks[2 * r] = (uint32_t)seed + (uint32_t)r * 0x9E3779B9u;
+    a.ks[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+  }
   a.flags = ctx->flags;
   a.out = *out;
 

@@ -91,6 +91,7 @@ struct RunArgs {
   int32_t R, rep0, K, T;
   int32_t flags;              // saim_params.flags
   uint64_t seed;
+  uint32_t ks[20];            // Philox key schedule of seed (saim_dev.cuh philox4x32_10_ks)
   double beta_max;
   saim_outputs out;           // device pointers
 };

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   ws->best_word[lane] = 0;
   __syncwarp();
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
+  uint32_t nflip = 0;                               // flips so far (warp-uniform)
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
   if (lane == 0) {
@@ -195,7 +196,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         }
       }
     }
-    cnt_add(ws, kCntFlips, 1);
+    ++nflip;
   };
 
   for (int k = 0; k < a.K; ++k) {
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         // Quiet carry-over: a group whose every spin was certified
         // saturated towards its value stays so while no spin flips -- the fields are unchanged and
         // beta_t only grows, so (2x-1) z only moves away from the threshold.
-        if (__all_sync(kFull, ws->gq[g] == ws->cnt[kCntFlips] + 1u)) continue;   // (vote: provably uniform)
+        if (__all_sync(kFull, ws->gq[g] == nflip + 1u)) continue;   // (vote: provably uniform)
         have_u = false;
         uint32_t nq = 0;
 #pragma unroll
@@ -347,8 +348,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #ifdef SAIM_STATS
         cnt_add(ws, kCntUncert, 1);
 #endif
-        // (re-read rather than kept live across the scan: registers are the limit at 28 warps/SM)
-        if (lane == 0) ws->gq[g] = m ? 0u : *reinterpret_cast<volatile uint32_t *>(&ws->cnt[kCntFlips]) + 1u;
+        if (lane == 0) ws->gq[g] = m ? 0u : nflip + 1u;
         if (m) handle_group(m);
       }
       cnt_add(ws, kCntSweeps, 1);
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   if (lane == 0 && a.out.counters) {
     unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
     atomicAdd(c + SAIM_CNT_DECISIONS, (unsigned long long)a.K * a.T * N);
-    atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)ws->cnt[kCntFlips]);
+    atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)nflip);
     atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)ws->cnt[kCntUnif]);
     atomicAdd(c + SAIM_CNT_FP64, (unsigned long long)ws->cnt[kCntFp64]);
     atomicAdd(c + SAIM_CNT_UNCERTIFIED, (unsigned long long)ws->cnt[kCntUncert]);
