@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   __syncwarp();
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
   uint32_t nflip = 0;                               // flips so far (warp-uniform)
+  uint32_t nunif = 0, nphil = 0;                    // uniforms drawn, lazy Philox calls x 32 (sweeps t >= 1)
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
   if (lane == 0) {
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
                 const uint4 u4 = philox_group_lazy(ws->key, g, lane, t, k, ws->srho);
                 ws->uw[0][lane] = u4.x; ws->uw[1][lane] = u4.y; ws->uw[2][lane] = u4.z; ws->uw[3][lane] = u4.w;
                 have_u = true;
-                cnt_add(ws, kCntPhilox, 32);
+                nphil += 32u;
               }
               w = ws->uw[bb][lane];
               l = logit_f32(w);
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           lo = L + 1;
           if (lo >= hi) break;
         }
-        if (drew) cnt_add(ws, kCntUnif, __popc(drew));
+        nunif += __popc(drew);
         return flipped;
       };
 
@@ -351,11 +352,13 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         if (lane == 0) ws->gq[g] = m ? 0u : nflip + 1u;
         if (m) handle_group(m);
       }
-      cnt_add(ws, kCntSweeps, 1);
       // Frozen anneal: a sweep in which every spin was certified
       // saturated towards its current value changed nothing; fields stay constant and beta only
       // grows, so every later sweep of this anneal is certified the same way -- x_k is final.
-      if (!active && freeze_exit && a.T >= 2) break;
+      if (!active && freeze_exit && a.T >= 2) {
+        cnt_add(ws, kCntSweeps, (uint32_t)(a.T - 1 - t));   // sweeps certified unchanged, not evaluated
+        break;
+      }
     }
     // ---- readout of x_k (Algorithm 1 "store feasible") ----
     int fpart = 0, load = 0;
@@ -430,12 +433,12 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
     atomicAdd(c + SAIM_CNT_DECISIONS, (unsigned long long)a.K * a.T * N);
     atomicAdd(c + SAIM_CNT_FLIPS, (unsigned long long)nflip);
-    atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)ws->cnt[kCntUnif]);
+    atomicAdd(c + SAIM_CNT_UNIFORMS, (unsigned long long)ws->cnt[kCntUnif] + nunif);
     atomicAdd(c + SAIM_CNT_FP64, (unsigned long long)ws->cnt[kCntFp64]);
     atomicAdd(c + SAIM_CNT_UNCERTIFIED, (unsigned long long)ws->cnt[kCntUncert]);
     atomicAdd(c + SAIM_CNT_FEASIBLE, (unsigned long long)ws->nfeas);
-    atomicAdd(c + SAIM_CNT_PHILOX, (unsigned long long)ws->cnt[kCntPhilox]);
-    atomicAdd(c + SAIM_CNT_SWEEPS, (unsigned long long)ws->cnt[kCntSweeps] + (a.T >= 2 ? (unsigned long long)a.K : 0ull));
+    atomicAdd(c + SAIM_CNT_PHILOX, (unsigned long long)ws->cnt[kCntPhilox] + nphil);
+    atomicAdd(c + SAIM_CNT_SWEEPS, (unsigned long long)a.K * a.T - ws->cnt[kCntSweeps]);
   }
 }
 
