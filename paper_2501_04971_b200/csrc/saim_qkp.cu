@@ -49,7 +49,6 @@ __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
 // Per-warp cold state in shared memory (kept out of the register file: the hot loop runs at
 // 28 warps/SM, i.e. <= 72 registers per thread).
 struct WarpState {
-  uint32_t gq[8];                  // group g was certified quiet when the flip count was gq[g] - 1
   float k1s, k2s, k3s;             // per unit t: K1 = t*bstep*c_o, K2 = t*bstep*c_p, K3 = t*bstep*c_l*Lambda
   float e0s, e1s;                  // scan error bound per unit t: e(A) = t*(e0s + e1s*A)
   float pad;
@@ -160,6 +159,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   __syncwarp();
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
   uint32_t nflip = 0;                               // flips so far (warp-uniform)
+  uint32_t qmask = 0;                               // groups certified quiet since the last flip
   uint32_t nunif = 0, nphil = 0;                    // uniforms drawn, lazy Philox calls x 32 (sweeps t >= 1)
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     ++nflip;
+    qmask = 0u;                                     // every quiet certificate is void after a flip
   };
 
   for (int k = 0; k < a.K; ++k) {
@@ -228,8 +229,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
-    if (lane < 8) ws->gq[lane] = 0u;                    // new Lambda_k: every group is scanned again
-    __syncwarp();
+    qmask = 0u;                                         // new Lambda_k: every group is scanned again
     for (int t = t0; t < a.T; ++t) {
       const float tf = (a.T >= 2) ? (float)t : 1.0f;     // exact
       bool active = false;                            // any non-quiet lane in this sweep?
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         // Quiet carry-over: a group whose every spin was certified
         // saturated towards its value stays so while no spin flips -- the fields are unchanged and
         // beta_t only grows, so (2x-1) z only moves away from the threshold.
-        if (__all_sync(kFull, ws->gq[g] == nflip + 1u)) continue;   // (vote: provably uniform)
+        if ((qmask >> g) & 1u) continue;
         have_u = false;
         uint32_t nq = 0;
 #pragma unroll
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #ifdef SAIM_STATS
         cnt_add(ws, kCntUncert, 1);
 #endif
-        if (lane == 0) ws->gq[g] = m ? 0u : nflip + 1u;
+        if (!m) qmask |= 1u << g;
         if (m) handle_group(m);
       }
       // Frozen anneal: a sweep in which every spin was certified
