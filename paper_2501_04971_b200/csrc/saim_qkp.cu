@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const int N = Hp->N;
   const int NB = (N + 31) >> 5;                      // NB <= NPL + 2
   const int NG = (NB + 3) >> 2;
+  const uint32_t allg = (1u << NG) - 1u;             // NG <= 5
   const bool has_con = a.M > 0;
 
   // x = 0: phi_i = -c_i, so (2x-1) phi = c_i; (2x-1) A = -A.
@@ -336,11 +337,14 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         }
       };
 
-      for (g = 0; g < NG; ++g) {
-        // Quiet carry-over: a group whose every spin was certified
-        // saturated towards its value stays so while no spin flips -- the fields are unchanged and
-        // beta_t only grows, so (2x-1) z only moves away from the threshold.
-        if ((qmask >> g) & 1u) continue;
+      // Quiet carry-over: a group whose every spin was certified
+      // saturated towards its value stays so while no spin flips -- the fields are unchanged and
+      // beta_t only grows, so (2x-1) z only moves away from the threshold.  Only the groups not
+      // so certified are visited; a flip voids every certificate, so all later groups follow.
+      uint32_t todo = allg & ~qmask;
+      while (todo) {
+        g = __ffs(todo) - 1;
+        todo &= todo - 1u;
         have_u = false;
         uint32_t nq = 0;
 #pragma unroll
@@ -349,8 +353,13 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #ifdef SAIM_STATS
         cnt_add(ws, kCntUncert, 1);
 #endif
-        if (!m) qmask |= 1u << g;
-        if (m) handle_group(m);
+        if (!m) {
+          qmask |= 1u << g;
+        } else {
+          const uint32_t nf0 = nflip;
+          handle_group(m);
+          if (nflip != nf0) todo = allg & ~((2u << g) - 1u);
+        }
       }
       // Frozen anneal: a sweep in which every spin was certified
       // saturated towards its current value changed nothing; fields stay constant and beta only
