@@ -76,11 +76,13 @@ typedef struct {
 #define SAIM_FLAG_NO_FREEZE_EXIT 1
 /* Kernel selection for linear objectives with M >= 2 constraints (MKP).  Default: the
  * outcome-tree kernel with L = 2 lanes per replica for M <= 8, the lane-per-replica lockstep
- * kernel for M > 8 (the faster one on B200).  These flags force the lockstep kernel or the
- * outcome tree with a given L.  All produce identical results. */
+ * kernel for M > 8 (the faster one on B200 for each).  These flags force the lockstep kernel,
+ * the outcome tree with a given L, or the row-split kernel (each replica's constraint rows over
+ * 2 lanes; honoured for M > 8 only).  At most one may be set.  All give identical results. */
 #define SAIM_FLAG_MKP_LOCKSTEP 2
 #define SAIM_FLAG_MKP_L2 4
 #define SAIM_FLAG_MKP_L4 8
+#define SAIM_FLAG_MKP_SPLIT2 16
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),

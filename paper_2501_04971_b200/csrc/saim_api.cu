@@ -28,6 +28,8 @@ int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blo
 cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
 int mkpt_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, int L, uint32_t *per_warp, int *max_wpc);
 cudaError_t mkpt_launch(const RunArgs &a, int n_inst, int MM, int L, int wpc, uint32_t per_warp, cudaStream_t st);
+int mkps_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, uint32_t *per_warp, int *max_wpc);
+cudaError_t mkps_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
 int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 }  // namespace saim
 
@@ -56,6 +58,7 @@ struct saim_ctx {
   int npl = 0, qb = 0;  // QKP
   int lanes = 32;       // lanes per replica (QKP: 32; MKP: 1 lockstep, L = 2 or 4 outcome tree)
   int mm = 0;           // MKP padded constraint count
+  int mkp_kind = 0;     // MKP kernel: 0 lockstep, 1 outcome tree, 2 row split
   uint32_t per_warp = 0;
   int N_max = 0, n_slack_max = 0;
   int smem_bytes = 0, max_wpc = 32, sm_count = 148;
@@ -97,8 +100,8 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     return fail(SAIM_EINVAL, "missing c/A/b/P array");
   if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
   if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
-  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) ||
-      __builtin_popcount(par->flags & (SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) > 1)
+  const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2;
+  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
     return fail(SAIM_EINVAL, "unknown or conflicting flags 0x%x", par->flags);
 
   if (M > 1 && prob->Q)
@@ -269,22 +272,37 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     const int MM = ctx->mm;
     const MkpLayout L = mkp_layout(n, MM);
     ctx->smem_bytes = (int)(L.bytes + ctx->per_warp);
-    // Default (measured on B200): outcome tree with L = 2 for M <= 8 (config 3:
-    // 1.15x the lockstep kernel), lockstep for larger M (config 4: 1.7x the tree).
+    // Default (measured on B200): outcome tree with L = 2 for M <= 8, the
+    // lockstep kernel for M > 8; the row split (M > 8) only on request.
     const bool tree = (ctx->flags & (SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) ||
                       (!(ctx->flags & SAIM_FLAG_MKP_LOCKSTEP) && M <= 8);
+    const bool split = !tree && MM >= 16 && (ctx->flags & SAIM_FLAG_MKP_SPLIT2);
     if (tree) {   // outcome-tree kernel (saim_mkp_tree.cu)
       const int lanes = (ctx->flags & SAIM_FLAG_MKP_L4) ? 4 : 2;
       uint32_t pw = 0;
       int wpc = 0;
       if (mkpt_plan(M, ctx->N_max, smem_optin, MM, L.bytes, lanes, &pw, &wpc) == 0) {
         ctx->lanes = lanes;
+        ctx->mkp_kind = 1;
         ctx->per_warp = pw;
         ctx->max_wpc = wpc;
         ctx->smem_bytes = (int)(L.bytes + pw);
       } else if (ctx->flags & (SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) {
         delete ctx;
         return fail(SAIM_ESMEM, "MKP outcome-tree kernel (L=%d) does not fit shared memory", lanes);
+      }
+    } else if (split) {   // row-split kernel (saim_mkp_split.cu)
+      uint32_t pw = 0;
+      int wpc = 0;
+      if (mkps_plan(M, ctx->N_max, smem_optin, MM, L.bytes, &pw, &wpc) == 0) {
+        ctx->lanes = 2;
+        ctx->mkp_kind = 2;
+        ctx->per_warp = pw;
+        ctx->max_wpc = wpc;
+        ctx->smem_bytes = (int)(L.bytes + pw);
+      } else if (ctx->flags & SAIM_FLAG_MKP_SPLIT2) {
+        delete ctx;
+        return fail(SAIM_ESMEM, "MKP row-split kernel does not fit shared memory");
       }
     }
     blob.assign((size_t)S * ctx->blob_bytes, 0);
@@ -384,7 +402,7 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
     e = qkp_launch(ctx->npl, ctx->qb, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
-  } else if (ctx->lanes == 1) {
+  } else if (ctx->mkp_kind == 0) {
     const long long warps = (long long)((R + 31) / 32) * ctx->n_inst;   // 32 replicas per warp (lockstep)
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
@@ -396,7 +414,8 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     const int ctas_inst = std::max(1, ctx->sm_count / ctx->n_inst);
     int wpc = (warps_inst + ctas_inst - 1) / ctas_inst;
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
-    e = mkpt_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st);
+    if (ctx->mkp_kind == 1) e = mkpt_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st);
+    else e = mkps_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st);
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SAIM_OK;

@@ -73,6 +73,13 @@ inline __host__ __device__ uint32_t mkp_band_stride(int n) { return align16u((ui
 inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM) {
   return align16u((uint32_t)WN * 128u) + 128u * 128u + (uint32_t)MM * 256u;
 }
+// Per-warp shared memory of the row-split kernel with S lanes per replica (G = 32/S replicas):
+// x bits [WN][G] words, logits of the current 128-spin group [128][G] floats, Lambda of each
+// lane's MM/S rows [MM/S][32 lanes] int64.
+inline __host__ __device__ uint32_t mkps_warp_bytes(int WN, int S, int MM) {
+  const uint32_t G = 32u / (uint32_t)S;
+  return align16u((uint32_t)WN * G * 4u) + 128u * G * 4u + (uint32_t)(MM / S) * 256u;
+}
 // Per-warp shared memory of the outcome-tree kernel with L lanes per replica (G = 32/L replica
 // groups): x bits [WN][G] words, logits of the current 128-spin group [128][G] floats, Lambda
 // [MM][G] int64.

@@ -223,9 +223,9 @@ def _mkp(n, m, t, seed):
     return si.mkp(n, m, t, [88, n, m, seed])
 
 
-# MKP kernel variants: default (outcome tree, L by M), lockstep, outcome tree with L = 2 and 4
-MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("tree_L2", 4), ("tree_L4", 8)]
-MKP_LANES = {0: None, 2: 1, 4: 2, 8: 4}
+# MKP kernel variants: default (outcome tree L = 2 for M <= 8, lockstep for M > 8), lockstep,
+# outcome tree with L = 2 and 4, row split over 2 lanes (honoured for M > 8; else the default)
+MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("tree_L2", 4), ("tree_L4", 8), ("split2", 16)]
 
 
 @pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
@@ -236,7 +236,8 @@ def test_mkp_parity_small(P, n, m, variant):
     p = _mkp(n, m, 0.5, 1)
     g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=40, K=4, T=30, flags=variant)
     assert g["info"]["kernel"] == 2
-    want = MKP_LANES[variant] or (2 if m <= 8 else 1)
+    default = 2 if m <= 8 else 1
+    want = {0: default, 2: 1, 4: 2, 8: 4, 16: 2}[variant]
     assert g["info"]["lanes_per_replica"] == want
 
 
@@ -253,15 +254,16 @@ def test_mkp_kernels_agree_on_counters(P):
     (flips, feasible samples, Philox calls) agree exactly.  ('uniforms' is not compared: whether a
     spin within a rounding margin of saturation counts as having drawn u depends on each kernel's
     error bound; the decision itself is certified either way.)"""
-    p = _mkp(100, 5, 0.5, 21)
-    Q, c, A, b = si.stack([p])
-    runs = [gpu_run(P, Q, c, A, b, [si.paper_P(p, 5.0)], 0.05, 50.0, 3, 70, 6, 60, flags=v) for _, v in MKP_VARIANTS]
-    for r in runs[1:]:
-        for k in ["tr_x", "tr_f", "tr_feas", "tr_r", "tr_lam", "best_f", "best_k", "best_x", "n_feasible",
-                  "final_x", "final_lam", "inst_best"]:
-            assert np.array_equal(runs[0][k], r[k]), k
-        for k in ["decisions", "flips", "sweeps", "feasible", "philox", "uncertified"]:
-            assert runs[0]["counters"][k] == r["counters"][k], k
+    for p in (_mkp(100, 5, 0.5, 21), _mkp(60, 12, 0.5, 22)):
+        Q, c, A, b = si.stack([p])
+        runs = [gpu_run(P, Q, c, A, b, [si.paper_P(p, 5.0)], 0.05, 50.0, 3, 70, 6, 60, flags=v)
+                for _, v in MKP_VARIANTS]
+        for r in runs[1:]:
+            for k in ["tr_x", "tr_f", "tr_feas", "tr_r", "tr_lam", "best_f", "best_k", "best_x", "n_feasible",
+                      "final_x", "final_lam", "inst_best"]:
+                assert np.array_equal(runs[0][k], r[k]), k
+            for k in ["decisions", "flips", "sweeps", "feasible", "philox", "uncertified"]:
+                assert runs[0]["counters"][k] == r["counters"][k], k
 
 
 @pytest.mark.parametrize("variant", [0, 2], ids=["default", "lockstep"])
@@ -272,12 +274,13 @@ def test_mkp_parity_config3_sampled(P, variant):
              reps=[0, 2047], flags=variant)
 
 
-def test_mkp_parity_config4_sampled(P):
+@pytest.mark.parametrize("variant", [0, 16], ids=["default", "split2"])
+def test_mkp_parity_config4_sampled(P, variant):
     """Config 4 shape (64 instances x 256 replicas, n=500, M=30) with K reduced to 4 so the
     oracle can replay sampled replicas; the launch configuration is the full one."""
     cfg = si.config_instances(4)
     g = run_both(P, cfg.instances[:8], cfg.P[:8], cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=4, T=cfg.T,
-                 reps=[0, 255])
+                 reps=[0, 255], flags=variant)
     assert g["info"]["kernel"] == 2
 
 
@@ -320,5 +323,11 @@ def test_degenerate_problems(P):
     m = _mkp(30, 3, 0.5, 4)
     m.A[1, :] = 0
     m.b[1] = 7
-    for v in (0, 2, 4, 8):
+    for v in (0, 2, 4, 8, 16):
         run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=19, R=32, K=3, T=20, flags=v)
+    # M > 8 with a row of zero weights in the second lane's half (row split)
+    m = _mkp(30, 12, 0.5, 5)
+    m.A[10, :] = 0
+    m.b[10] = 5
+    for v in (0, 2, 16):
+        run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=20, R=24, K=3, T=20, flags=v)
