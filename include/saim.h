@@ -102,6 +102,9 @@ typedef struct {
   uint32_t *tr_x;          /* [n_inst][R][K][WN]  full sample x_k incl. slack bits */
   uint32_t *final_x;       /* [n_inst][R][WN]     state after the last sweep */
   int64_t *final_lam;      /* [n_inst][R][M]      Lambda_K */
+  uint32_t *rep_flips;     /* [n_inst][R]         spin flips of each replica's chain over the whole run
+                            * (incl. the beta = 0 sweeps): a fingerprint of the full trajectory, not
+                            * only of the K readouts (the oracle counts the same) */
 } saim_outputs;
 
 typedef struct {

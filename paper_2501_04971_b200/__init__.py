@@ -45,7 +45,7 @@ class _Params(C.Structure):
 
 
 _OUT_FIELDS = ["best_f", "best_x", "best_k", "n_feasible", "inst_best", "counters",
-               "tr_f", "tr_feas", "tr_r", "tr_lam", "tr_x", "final_x", "final_lam"]
+               "tr_f", "tr_feas", "tr_r", "tr_lam", "tr_x", "final_x", "final_lam", "rep_flips"]
 
 
 class _Outputs(C.Structure):
@@ -163,7 +163,8 @@ class Solver:
                        tr_x=torch.empty((S, R, K, WN), dtype=torch.int32, device=dev))
         if final:
             out.update(final_x=torch.empty((S, R, WN), dtype=torch.int32, device=dev),
-                       final_lam=torch.empty((S, R, M), dtype=torch.int64, device=dev))
+                       final_lam=torch.empty((S, R, M), dtype=torch.int64, device=dev),
+                       rep_flips=torch.empty((S, R), dtype=torch.int32, device=dev))
         return out
 
     def run(self, seed: int, R: int, K: int, T: int, rep0: int = 0, trace: bool = False, final: bool = False,

@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       for (int w = 0; w < a.WN; ++w) a.out.final_x[ri * a.WN + w] = xw[32 * w];
     if (a.out.final_lam)
       for (int m = 0; m < M; ++m) a.out.final_lam[ri * M + m] = Lam[32 * m];
+    if (a.out.rep_flips) a.out.rep_flips[ri] = c_flips;
   }
   // per-instance best (f << 20 | rho): warp min, one atomic
   long long key_best = (live && best_k >= 0) ? ((best_f << 20) | (long long)rho) : LLONG_MAX;

@@ -358,8 +358,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1) saim_mkp_split_kernel(const 
 
   // ---- outputs ----
   const size_t ri = (size_t)s * a.R + ridx;
+  const uint32_t rflips = c_flips + __shfl_xor_sync(kFull, c_flips, 1);   // items (lead) + own slack rows
   if (live) {
     if (lead) {
+      if (a.out.rep_flips) a.out.rep_flips[ri] = rflips;
       a.out.best_f[ri] = best_f;
       a.out.best_k[ri] = best_k;
       a.out.n_feasible[ri] = nfeas;

@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kTreeThreads, 1) saim_mkp_tree_kernel(const Ru
       a.out.best_f[ri] = best_f;
       a.out.best_k[ri] = best_k;
       a.out.n_feasible[ri] = nfeas;
+      if (a.out.rep_flips) a.out.rep_flips[ri] = c_flips;     // lane 0 counts the whole replica's flips
     }
     if (best_k < 0)
       for (int w = ell; w < Wn; w += L) a.out.best_x[ri * a.Wn + w] = 0u;

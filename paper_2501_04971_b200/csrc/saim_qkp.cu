@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const int N = Hp->N;
   const int NB = (N + 31) >> 5;                      // NB <= NPL + 2
   const int NG = (NB + 3) >> 2;
-  const uint32_t allg = (1u << NG) - 1u;             // NG <= 5
+  const uint32_t allb = (1u << NB) - 1u;             // NB <= 18 (padding blocks are never visited)
   const bool has_con = a.M > 0;
 
   // x = 0: phi_i = -c_i, so (2x-1) phi = c_i; (2x-1) A = -A.
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   __syncwarp();
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
   uint32_t nflip = 0;                               // flips so far (warp-uniform)
-  uint32_t qmask = 0;                               // groups certified quiet since the last flip
+  uint32_t qmask = 0;                               // blocks certified quiet since the last flip
   uint32_t nunif = 0, nphil = 0;                    // uniforms drawn, lazy Philox calls x 32 (sweeps t >= 1)
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
@@ -331,34 +331,36 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           uint32_t nq = 0;
 #pragma unroll
           for (int bb = 0; bb < 4; ++bb)
-            if (bb >= bstart) scan_one(nq, 4 * g + bb, bb);
+            if (bb >= bstart && 4 * g + bb < NB) scan_one(nq, 4 * g + bb, bb);
           m = __reduce_or_sync(kFull, nq);
           if (!m) return;
         }
       };
 
-      // Quiet carry-over: a group whose every spin was certified
+      // Quiet carry-over: a block whose every spin was certified
       // saturated towards its value stays so while no spin flips -- the fields are unchanged and
-      // beta_t only grows, so (2x-1) z only moves away from the threshold.  Only the groups not
-      // so certified are visited; a flip voids every certificate, so all later groups follow.
-      uint32_t todo = allg & ~qmask;
+      // beta_t only grows, so (2x-1) z only moves away from the threshold.  Only the blocks not
+      // so certified are scanned (4 per group in one pass); a flip voids every certificate, so
+      // all later blocks follow.
+      uint32_t todo = allb & ~qmask;
       while (todo) {
-        g = __ffs(todo) - 1;
-        todo &= todo - 1u;
+        g = (__ffs(todo) - 1) >> 2;
+        const uint32_t gb = (todo >> (4 * g)) & 15u;        // blocks of group g to scan
+        todo &= ~(15u << (4 * g));
         have_u = false;
         uint32_t nq = 0;
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) scan_one(nq, 4 * g + bb, bb);
+        for (int bb = 0; bb < 4; ++bb)
+          if ((gb >> bb) & 1u) scan_one(nq, 4 * g + bb, bb);
         const uint32_t m = __reduce_or_sync(kFull, nq);
 #ifdef SAIM_STATS
         cnt_add(ws, kCntUncert, 1);
 #endif
-        if (!m) {
-          qmask |= 1u << g;
-        } else {
+        qmask |= (gb & ~m) << (4 * g);                     // scanned and quiet: certified
+        if (m) {
           const uint32_t nf0 = nflip;
           handle_group(m);
-          if (nflip != nf0) todo = allg & ~((2u << g) - 1u);
+          if (nflip != nf0) todo = allb & ~((16u << (4 * g)) - 1u);
         }
       }
       // Frozen anneal: a sweep in which every spin was certified
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (ws->best_k >= 0 && a.out.inst_best)
       atomicMin(reinterpret_cast<long long *>(a.out.inst_best) + s, (ws->best_f << 20) | (long long)rho);
     if (has_con && a.out.final_lam) a.out.final_lam[ri] = ws->Lam;
+    if (a.out.rep_flips) a.out.rep_flips[ri] = nflip;
   }
   if (lane < a.Wn) a.out.best_x[ri * a.Wn + lane] = ws->best_word[lane];
   if (a.out.final_x) {

@@ -66,7 +66,7 @@ def compare(g, o, s, reps, N, K, M):
             assert np.array_equal(g["final_lam"][s, reps], o["final_lam"])
 
 
-def run_both(P, probs, Pens, eta, beta_max, seed, R, K, T, reps=None, rep0=0, flags=0):
+def run_both(P, probs, Pens, eta, beta_max, seed, R, K, T, reps=None, rep0=0, flags=0, block=None):
     Q, c, A, b = si.stack(probs)
     g = gpu_run(P, Q, c, A, b, Pens, eta, beta_max, seed, R, K, T, rep0=rep0, flags=flags)
     assert g["counters"]["uncertified"] == 0
@@ -83,6 +83,12 @@ def run_both(P, probs, Pens, eta, beta_max, seed, R, K, T, reps=None, rep0=0, fl
             for r in rr:                       # sampled replicas, one oracle call each (global index)
                 o = op.run(seed, 1, K, T, rep0=rep0 + r, trace=True, final=True)
                 compare(g, o, s, [r], op.N, K, pr.M)
+                assert int(g["rep_flips"][s, r]) == o["counters"]["flips"], "trajectory (flip count) differs"
+            if block is not None:              # a contiguous block of replicas, oracle threaded over it
+                b0, nb = block
+                o = op.run(seed, nb, K, T, rep0=rep0 + b0, trace=True, final=True)
+                compare(g, o, s, list(range(b0, b0 + nb)), op.N, K, pr.M)
+                assert int(g["rep_flips"][s, b0:b0 + nb].sum()) == o["counters"]["flips"], "trajectories differ"
     if reps is None:
         assert g["counters"]["flips"] == flips
     assert g["counters"]["decisions"] == sum(K * T * R * g["inst"][s]["N"] for s in range(len(probs)))
@@ -188,14 +194,15 @@ def test_parity_config1_sampled(P):
     the oracle recomputes sampled replicas one by one."""
     cfg = si.config_instances(1)
     run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
-             reps=[0, 377, 1023])
+             reps=[0, 377, 1023], block=(512, 32))
 
 
 def test_parity_config2_sampled(P):
-    """BASELINE config 2 (headline) at full size; sampled replicas against the oracle."""
+    """BASELINE config 2 (headline) at full size; sampled replicas (the first, the last and a
+    contiguous block of 48) against the oracle."""
     cfg = si.config_instances(2)
     run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
-             reps=[0, 4095])
+             reps=[0, 4095], block=(1024, 48))
 
 
 @pytest.mark.parametrize("cfg_idx", [0, 1])

@@ -10,7 +10,7 @@ for r in $(seq $N); do
     python tools/bench_all.py --configs $CF --reps 3 | python -c "
 import json,sys
 for l in sys.stdin:
-    d=json.loads(l); print(d['config'], '$(basename $v)', round(d['seconds']*1e3,2), 'ms', d['counters']['flips'])"
+    d=json.loads(l); print(d['config'], '$(basename $v)', round(d['seconds']*1e3,2), 'ms', d['counters']['flips'], d['counters']['philox'], d['counters']['uniforms'])"
   done
 done
 cp /tmp/ab_orig.so $LIB
