@@ -83,6 +83,9 @@ typedef struct {
 #define SAIM_FLAG_MKP_L2 4
 #define SAIM_FLAG_MKP_L4 8
 #define SAIM_FLAG_MKP_SPLIT2 16
+/* QKP kernel: disable the hot-block loop (sweeps in which a single uncertified block flips nothing
+ * run back to back without the general block machinery).  Results are identical either way. */
+#define SAIM_FLAG_QKP_NO_HOT_LOOP 32
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),

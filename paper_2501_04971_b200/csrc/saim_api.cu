@@ -101,7 +101,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
   if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
   if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
   const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2;
-  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
+  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_QKP_NO_HOT_LOOP | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
     return fail(SAIM_EINVAL, "unknown or conflicting flags 0x%x", par->flags);
 
   if (M > 1 && prob->Q)

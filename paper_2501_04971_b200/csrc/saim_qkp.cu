@@ -27,6 +27,19 @@
 
 #include "saim_dev.cuh"
 
+#ifdef SAIM_PROF
+// Development profiling build only (-DSAIM_PROF): per-sweep clock64 totals by phase of the anneal.
+__device__ unsigned long long saim_prof[8];
+extern "C" int saim_prof_read(unsigned long long *h, int reset) {
+  cudaMemcpyFromSymbol(h, saim_prof, sizeof(saim_prof));
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(saim_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 namespace saim {
 
 namespace {
@@ -61,6 +74,9 @@ struct WarpState {
   uint2 key;                        // Philox key (lo32 seed, hi32 seed)
   uint32_t srho;                    // (s << 20) | rho
   uint32_t uw[4][32];               // lazily drawn words of the current group, per lane
+#ifdef SAIM_PROF
+  unsigned long long prof[8];
+#endif
 };
 enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps };
 
@@ -153,6 +169,9 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     ws->best_f = LLONG_MAX;
     ws->best_k = -1;
     ws->nfeas = 0;
+#ifdef SAIM_PROF
+    for (int i = 0; i < 8; ++i) ws->prof[i] = 0;
+#endif
 #pragma unroll
     for (int i = 0; i < 6; ++i) ws->cnt[i] = 0;
   }
@@ -230,8 +249,73 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
+    const bool hot_loop = a.T >= 2 && !(a.flags & SAIM_FLAG_QKP_NO_HOT_LOOP);
     qmask = 0u;                                         // new Lambda_k: every group is scanned again
     for (int t = t0; t < a.T; ++t) {
+#ifdef SAIM_PROF
+      const long long prof_c0 = clock64();
+#endif
+      // ---- Hot-block loop ----
+      // Every block but one (b) is certified quiet: those keep their spins whatever happens in b
+      // as long as nothing flips.  While b's own decisions flip nothing, its fields stay constant
+      // and a whole sweep is just b's 32 decisions: run such sweeps back to back here.  The sweep
+      // in which b would flip a spin (or turns quiet) is left to the general path below, which
+      // re-derives the same decisions from the same state and uniforms.  The uniforms of b's
+      // unsaturated lanes [plo, plo + pw) for the next pS = 32 / pw sweeps come from one
+      // warp-wide Philox call, lane j holding word bb of spin lane plo + j % pw, sweep pt0 + j / pw.
+      if (hot_loop && qmask != allb && !((allb & ~qmask) & ((allb & ~qmask) - 1u))) {
+        const int b = __ffs(allb & ~qmask) - 1;
+        const int bb = b & 3, gq = b >> 2;
+        const float A = sAl[32 * b];
+        const bool xb = (xm >> b) & 1u;
+        const float sg = xb ? -1.0f : 1.0f;
+        const float phib = -sg * phs[32 * b];
+        const float v = fmaf(A, sg, r2);
+        const bool mine = lane < N - 32 * b;
+        const float k1s = ws->k1s, k2s = ws->k2s, k3s = ws->k3s;
+        uint32_t wreg = 0, pmask = 0;
+        int pt0 = 0, plo = 0, pw = 32, pS = 0;
+        for (; t < a.T; ++t) {
+          const float tf = (float)t;
+          const float K1 = tf * k1s, K2 = tf * k2s, K3 = tf * k3s;
+          const float AK2 = A * K2, AK3 = A * K3;
+          const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));
+          const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
+          const bool sat = fabsf(z) * kZScale - S > kSatThr20;
+          int nx = z > 0.0f;
+          const uint32_t need = __ballot_sync(kFull, mine && !sat);
+          if (!need) break;                               // b quiet (or flipping): general path
+          if ((need & ~pmask) || t - pt0 >= pS) {
+            plo = __ffs(need) - 1;
+            pw = 32 - __clz(need) - plo;
+            // sj = lane / pw, exact: (lane + 1/2) / pw is >= 1/(2 pw) away from an integer
+            const int sj = (int)(((float)lane + 0.5f) * __frcp_rn((float)pw));
+            const uint4 u4 = philox_group_lazy(ws->key, gq, plo + lane - sj * pw, t + sj, k, ws->srho);
+            wreg = sel4(u4, bb);
+            pt0 = t;
+            pS = (int)(32.5f * __frcp_rn((float)pw));
+            pmask = (pw == 32) ? kFull : (((1u << pw) - 1u) << plo);
+            nphil += 32u;
+          }
+          const uint32_t w = __shfl_sync(kFull, wreg, ((t - pt0) * pw + lane - plo) & 31);
+          const float l = logit_f32(w);
+          const float el = kLogitAbs + kLogitRel * fabsf(l);
+          if (mine && !sat) {
+            const float d = z - l;
+            if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
+              nx = d > 0.0f;
+            } else {
+              const int rs = decide_fp64(phib, v, A, t, Hp, ws, w);
+              nx = rs & 1;
+              atomicAdd(&ws->cnt[kCntFp64], 1u);
+              if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
+            }
+          }
+          if (__ballot_sync(kFull, mine && nx != (int)xb)) break;   // a flip: general path
+          nunif += __popc(need);
+        }
+        if (t >= a.T) break;
+      }
       const float tf = (a.T >= 2) ? (float)t : 1.0f;     // exact
       bool active = false;                            // any non-quiet lane in this sweep?
       // fp32 sweep constants (two roundings each; the bounds below keep a >= 3x margin)
@@ -366,6 +450,13 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // Frozen anneal: a sweep in which every spin was certified
       // saturated towards its current value changed nothing; fields stay constant and beta only
       // grows, so every later sweep of this anneal is certified the same way -- x_k is final.
+#ifdef SAIM_PROF
+      if (lane == 0) {
+        const int pb = t < a.T / 10 ? 0 : (t < (3 * a.T) / 10 ? 1 : 2);
+        ws->prof[pb] += (unsigned long long)(clock64() - prof_c0);
+        ws->prof[4 + pb] += 1ull;
+      }
+#endif
       if (!active && freeze_exit && a.T >= 2) {
         cnt_add(ws, kCntSweeps, (uint32_t)(a.T - 1 - t));   // sweeps certified unchanged, not evaluated
         break;
@@ -441,6 +532,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     }
     if (lane < a.WN) a.out.final_x[ri * a.WN + lane] = myword;
   }
+#ifdef SAIM_PROF
+  if (lane == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(&saim_prof[i], ws->prof[i]);
+#endif
   if (lane == 0 && a.out.counters) {
     unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
     atomicAdd(c + SAIM_CNT_DECISIONS, (unsigned long long)a.K * a.T * N);

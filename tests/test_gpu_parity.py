@@ -223,6 +223,23 @@ def test_freeze_exit_is_exact(P, cfg_idx):
     assert on["counters"]["sweeps"] <= off["counters"]["sweeps"]
 
 
+@pytest.mark.parametrize("cfg_idx", [0, 1, 2])
+def test_qkp_hot_loop_is_exact(P, cfg_idx):
+    """The hot-block loop changes how sweeps are executed, not what
+    they decide: every output, every replica's flip count and the data-determined counters agree
+    with the general path alone."""
+    cfg = si.config_instances(cfg_idx)
+    Q, c, A, b = si.stack(cfg.instances)
+    R, K = (64, cfg.K) if cfg_idx == 0 else (512, 8)
+    on = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 6, R, K, cfg.T)
+    off = gpu_run(P, Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, 6, R, K, cfg.T, flags=P.FLAG_QKP_NO_HOT_LOOP)
+    for k in ["tr_x", "tr_f", "tr_feas", "tr_r", "tr_lam", "best_f", "best_k", "best_x", "n_feasible",
+              "final_x", "final_lam", "inst_best", "rep_flips"]:
+        assert np.array_equal(on[k], off[k]), k
+    for k in ["decisions", "flips", "uniforms", "feasible", "uncertified", "sweeps"]:
+        assert on["counters"][k] == off["counters"][k], k
+
+
 # ---------------------------------------------------------------------------------------------
 # MKP kernel (linear objective, M >= 2; BASELINE configs 3-4)
 
