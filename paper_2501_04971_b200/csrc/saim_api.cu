@@ -66,6 +66,7 @@ struct saim_ctx {
   double beta_max = 0, eta = 0;
   int flags = 0;
   long long r_abs_max = 0;
+  int r_tol = 0;        // QKP certificate tolerance D (min over instances)
   unsigned char *d_blob = nullptr;
   InstHdr *d_hdr = nullptr;
   std::vector<InstHdr> hdr;
@@ -182,6 +183,14 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
       }
       h.v_bound = 2.0 * (double)rmax + (double)amax;
       h.r_bound = (double)rmax;
+      // QKP quiet certificates hold for |r - r_cert| <= D: the tolerance widens the scan threshold
+      // by 2 beta c_p D |A_i| <= 1 (of ln(2^24-1) = 16.6) for the heaviest item.
+      long long aitem = 0;
+      for (int k = 0; k < M; ++k)
+        for (int j = 0; j < n; ++j) aitem = std::max(aitem, (long long)A[(size_t)k * n + j]);
+      const double dt = (h.c_p > 0 && aitem > 0) ? std::floor(0.5 / (par->beta_max * h.c_p * (double)aitem)) : 0.0;
+      const int rt = (int)std::min(dt, (double)(1 << 20));
+      ctx->r_tol = (s == 0) ? rt : std::min(ctx->r_tol, rt);
     }
     ctx->N_max = std::max(ctx->N_max, h.N);
     ctx->n_slack_max = std::max(ctx->n_slack_max, n_slack);
@@ -392,6 +401,7 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     a.ks[2 * r + 1] = (uint32_t)(seed >> 32) + (uint32_t)r * 0xBB67AE85u;
   }
   a.flags = ctx->flags;
+  a.rtol2 = 2.0f * (float)ctx->r_tol;
   a.out = *out;
 
   saim_init_outputs<<<(ctx->n_inst + 255) / 256, 256, 0, st>>>(out->inst_best, ctx->n_inst, out->counters);

@@ -100,6 +100,7 @@ struct RunArgs {
   uint64_t seed;
   uint32_t ks[20];            // Philox key schedule of seed (saim_dev.cuh philox4x32_10_ks)
   double beta_max;
+  float rtol2;                // QKP: 2D, a quiet certificate holds while |2r - 2r_cert| <= 2D
   saim_outputs out;           // device pointers
 };
 

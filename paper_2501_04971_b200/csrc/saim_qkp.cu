@@ -164,7 +164,9 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     ws->k2s = (float)(bstep * Hp->c_p);
     ws->k3s = 0.0f;
     ws->e0s = (float)(bstep * Hp->c_o * Hp->phi_bound * 0x1p-20);
-    ws->e1s = (float)(bstep * Hp->c_p * Hp->v_bound * 0x1p-20);
+    // 2^-20 S error bound, plus the certificate tolerance: |2r - 2r_cert| <= 2D moves (2x-1) z by
+    // at most 2 K2 D |A| (margin 1.001 over the fp32 rounding of K2)
+    ws->e1s = (float)(bstep * Hp->c_p * (Hp->v_bound * 0x1p-20 + 1.001 * (double)a.rtol2));
     ws->Lam = 0;
     ws->best_f = LLONG_MAX;
     ws->best_k = -1;
@@ -200,7 +202,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       asg[32 * b] = -asg[32 * b];
     }
     const int j = 32 * b + L;
-    if (j < n) {
+    if (j < n) {                                    // an item flip moves phi: certificates void
+      qmask = 0u;
       const uint32_t *row = sQl + j * (QW * 32);
 #pragma unroll
       for (int w = 0; w < QW; ++w) {
@@ -218,7 +221,13 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       }
     }
     ++nflip;
-    qmask = 0u;                                     // every quiet certificate is void after a flip
+  };
+  // Quiet certificates are made with margin for any 2r within
+  // +-rtol2 of r2c, the value of 2r when they were made: blocks found quiet at another r replace
+  // the current certificates (the others are scanned again next sweep).
+  float r2c = 0.0f;
+  auto certify = [&](uint32_t bits) {
+    if (!qmask || r2 != r2c) { r2c = r2; qmask = bits; } else { qmask |= bits; }
   };
 
   for (int k = 0; k < a.K; ++k) {
@@ -440,11 +449,16 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #ifdef SAIM_STATS
         cnt_add(ws, kCntUncert, 1);
 #endif
-        qmask |= (gb & ~m) << (4 * g);                     // scanned and quiet: certified
+        if (gb & ~m) certify((gb & ~m) << (4 * g));        // scanned and quiet: certified
         if (m) {
           const uint32_t nf0 = nflip;
           handle_group(m);
-          if (nflip != nf0) todo = allb & ~((16u << (4 * g)) - 1u);
+          if (nflip != nf0) {
+            // item flips voided the certificates; slack flips only moved r -- the certificates
+            // hold while 2r stays within the tolerance (checked before a certified block is skipped)
+            if (fabsf(r2 - r2c) > a.rtol2) qmask = 0u;
+            todo = allb & ~qmask & ~((16u << (4 * g)) - 1u);
+          }
         }
       }
       // Frozen anneal: a sweep in which every spin was certified
@@ -506,7 +520,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       const double Lnew = (double)(Lam + rl);
       ws->Lam = Lam + rl;
       ws->k3s = (float)(ws->bstep * (Hp->c_l * Lnew));
-      ws->e1s = (float)(ws->bstep * (Hp->c_p * Hp->v_bound + Hp->c_l * fabs(Lnew)) * 0x1p-20);
+      ws->e1s = (float)(ws->bstep * ((Hp->c_p * Hp->v_bound + Hp->c_l * fabs(Lnew)) * 0x1p-20 +
+                                     1.001 * Hp->c_p * (double)a.rtol2));
     }
     __syncwarp();
   }
