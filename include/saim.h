@@ -86,6 +86,9 @@ typedef struct {
 /* QKP kernel: disable the hot-block loop (sweeps in which a single uncertified block flips nothing
  * run back to back without the general block machinery).  Results are identical either way. */
 #define SAIM_FLAG_QKP_NO_HOT_LOOP 32
+/* MKP lockstep kernel: no producer warps (each consumer warp draws its own logits).  Identical
+ * results either way. */
+#define SAIM_FLAG_MKP_NO_PRODUCER 64
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),

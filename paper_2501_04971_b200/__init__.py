@@ -24,6 +24,7 @@ FLAG_MKP_LOCKSTEP = 2      # MKP: lane-per-replica kernel instead of the outcome
 FLAG_MKP_L2 = 4            # MKP: outcome tree with 2 lanes per replica
 FLAG_MKP_L4 = 8            # MKP: outcome tree with 4 lanes per replica
 FLAG_MKP_SPLIT2 = 16       # MKP: constraint rows of a replica split over 2 lanes (M > 8)
+FLAG_MKP_NO_PRODUCER = 64  # MKP lockstep: consumer warps draw their own logits (identical results)
 FLAG_QKP_NO_HOT_LOOP = 32  # QKP: disable the hot-block loop (identical results)
 EXPORTS = ["saim_create", "saim_run", "saim_get_info", "saim_get_instance", "saim_destroy",
            "saim_last_error", "saim_selftest"]

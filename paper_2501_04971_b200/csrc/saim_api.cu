@@ -24,7 +24,7 @@ int qkp_npl_bucket(int npl);
 cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *max_wpc);
 cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st);
 int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
-             int *max_wpc);
+             int *max_wpc, uint32_t *per_warp_prod, int *max_wpc_prod);
 cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
 int mkpt_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, int L, uint32_t *per_warp, int *max_wpc);
 cudaError_t mkpt_launch(const RunArgs &a, int n_inst, int MM, int L, int wpc, uint32_t per_warp, cudaStream_t st);
@@ -60,6 +60,8 @@ struct saim_ctx {
   int mm = 0;           // MKP padded constraint count
   int mkp_kind = 0;     // MKP kernel: 0 lockstep, 1 outcome tree, 2 row split
   uint32_t per_warp = 0;
+  uint32_t per_warp_prod = 0;  // MKP lockstep with producer warps: per-consumer region, max consumers per CTA
+  int max_wpc_prod = 0;
   int N_max = 0, n_slack_max = 0;
   int smem_bytes = 0, max_wpc = 32, sm_count = 148;
   uint32_t blob_bytes = 0, a_off = 0, c_off = 0, x_off = 0;
@@ -102,7 +104,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
   if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
   if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
   const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2;
-  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_QKP_NO_HOT_LOOP | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
+  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_QKP_NO_HOT_LOOP | SAIM_FLAG_MKP_NO_PRODUCER | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
     return fail(SAIM_EINVAL, "unknown or conflicting flags 0x%x", par->flags);
 
   if (M > 1 && prob->Q)
@@ -274,7 +276,8 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     // ---------------- MKP kernel layout (saim_layout.h MkpLayout) ----------------
     ctx->kernel = 2;
     ctx->lanes = 1;
-    if (mkp_plan(n, M, ctx->N_max, smem_optin, &ctx->mm, &ctx->blob_bytes, &ctx->per_warp, &ctx->max_wpc) != 0) {
+    if (mkp_plan(n, M, ctx->N_max, smem_optin, &ctx->mm, &ctx->blob_bytes, &ctx->per_warp, &ctx->max_wpc,
+                 &ctx->per_warp_prod, &ctx->max_wpc_prod) != 0) {
       delete ctx;
       return fail(SAIM_ESMEM, "MKP instance (n=%d, M=%d, N=%d) does not fit shared memory", n, M, ctx->N_max);
     }
@@ -415,8 +418,11 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
   } else if (ctx->mkp_kind == 0) {
     const long long warps = (long long)((R + 31) / 32) * ctx->n_inst;   // 32 replicas per warp (lockstep)
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
-    wpc = std::max(1, std::min(wpc, ctx->max_wpc));
-    e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st);
+    // producer warps when the consumers still fit one wave with their partners
+    const bool prod = !(ctx->flags & SAIM_FLAG_MKP_NO_PRODUCER) && wpc <= ctx->max_wpc_prod;
+    a.mkp_prod = prod ? 1 : 0;
+    wpc = std::max(1, std::min(wpc, prod ? ctx->max_wpc_prod : ctx->max_wpc));
+    e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, prod ? ctx->per_warp_prod : ctx->per_warp, st);
   } else {
     // one CTA per SM: spread each instance's warps over floor(SMs / n_inst) CTAs
     const int G = 32 / ctx->lanes;

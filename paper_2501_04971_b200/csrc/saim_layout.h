@@ -70,8 +70,10 @@ inline __host__ __device__ MkpLayout mkp_layout(int n, int MM) {
 inline __host__ __device__ uint32_t mkp_band_stride(int n) { return align16u((uint32_t)(n + 1) * 4u) / 4u; }
 // Per-warp MKP shared memory (lockstep kernel): x bits [WN][32 lanes], logits of the current
 // 128-spin group [128][32] floats, Lambda [MM][32] int64.
-inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM) {
-  return align16u((uint32_t)WN * 128u) + 128u * 128u + (uint32_t)MM * 256u;
+// With producer warps (prod = 1): two logit buffers [2][128][32] (groups alternate by parity) and
+// the consumer/producer mbarriers full[2], empty[2] after Lambda.
+inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM, int prod = 0) {
+  return align16u((uint32_t)WN * 128u) + (prod ? 2u : 1u) * 128u * 128u + (uint32_t)MM * 256u + (prod ? 32u : 0u);
 }
 // Per-warp shared memory of the row-split kernel with S lanes per replica (G = 32/S replicas):
 // x bits [WN][G] words, logits of the current 128-spin group [128][G] floats, Lambda of each
@@ -100,6 +102,7 @@ struct RunArgs {
   uint64_t seed;
   uint32_t ks[20];            // Philox key schedule of seed (saim_dev.cuh philox4x32_10_ks)
   double beta_max;
+  int32_t mkp_prod;           // MKP lockstep: 1 = producer warps draw the logits
   float rtol2;                // QKP: 2D, a quiet certificate holds while |2r - 2r_cert| <= 2D
   saim_outputs out;           // device pointers
 };

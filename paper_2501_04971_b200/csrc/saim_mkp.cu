@@ -14,6 +14,7 @@
 // fp32 with a rigorous error bound; c_l Lambda_m is rounded once per iteration.
 // Decisions are certified exactly as in the QKP kernel: saturated test, fp32 logit band, fp64
 // slow path (counted when even that is not certain).
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <type_traits>
@@ -46,6 +47,25 @@ __device__ __forceinline__ float logit_signed(uint32_t w) {
   return (w >> 31) ? l : -l;
 }
 
+// mbarrier helpers for the consumer/producer pairs (shared::cta, one phase per buffer fill).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+
 template <int MM>
 struct MkpCfg {
   static constexpr int kThreads = MM <= 16 ? 512 : 256;
@@ -55,18 +75,33 @@ struct MkpCfg {
 
 // MM: padded constraint count (layout); MA <= MM: rows the arithmetic loops cover (= M for the
 // instantiated exact sizes, else MM with zero-padded rows).
-template <int MM, int MA>
+template <int MM, int MA, bool PROD>
 __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const RunArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t mbar;
 
   const int s = blockIdx.y;
-  bulk_stage(smem, a.blob + (size_t)s * a.blob_bytes, a.blob_bytes, &mbar);
-
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ridx = (blockIdx.x * (blockDim.x >> 5) + warp) * 32 + lane;
-  const int wfirst = (blockIdx.x * (blockDim.x >> 5) + warp) * 32;
-  if (wfirst >= a.R) return;                         // whole warp beyond R
+  // Producer warps (a.mkp_prod): the CTA's second half of warps draws the logits
+  // of the first half's replicas -- state-independent -- into double-buffered groups, so the
+  // consumers' instruction stream (one warp per SMSP: issue-limited per warp) is decisions only.
+  constexpr bool prod = PROD;                          // (a.mkp_prod selects this instantiation)
+  const int nc = prod ? (int)(blockDim.x >> 6) : (int)(blockDim.x >> 5);   // consumer warps per CTA
+  const bool producer = prod && warp >= nc;
+  const int cw = producer ? warp - nc : warp;          // consumer warp (own, or the partner's)
+  unsigned char *wbase = smem + a.blob_bytes + cw * mkp_warp_bytes(a.WN, MM, prod ? 1 : 0);
+  const uint32_t lbytes = (prod ? 2u : 1u) * 128u * 128u;
+  uint64_t *mb = reinterpret_cast<uint64_t *>(wbase + align16u(a.WN * 128u) + lbytes + MM * 256u);  // full[2], empty[2]
+  if (prod && !producer && lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mbar_init(mb + i, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  bulk_stage(smem, a.blob + (size_t)s * a.blob_bytes, a.blob_bytes, &mbar);   // (includes __syncthreads)
+
+  const int ridx = (blockIdx.x * nc + cw) * 32 + lane;
+  const int wfirst = (blockIdx.x * nc + cw) * 32;
+  if (wfirst >= a.R) return;                         // whole warp beyond R (its partner too)
   const bool live = ridx < a.R;                        // lanes beyond R compute but never write
   const int rho = a.rep0 + (live ? ridx : a.R - 1);
   const InstHdr *Hp = a.hdr + s;
@@ -78,10 +113,39 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + L.cint);
   const long long *sB = reinterpret_cast<const long long *>(smem + L.brow);
   const int32_t *sQ = reinterpret_cast<const int32_t *>(smem + L.qrow);
-  unsigned char *wbase = smem + a.blob_bytes + warp * mkp_warp_bytes(a.WN, MM);
   uint32_t *xw = reinterpret_cast<uint32_t *>(wbase) + lane;                            // word w: xw[32 w]
-  float *lt = reinterpret_cast<float *>(wbase + align16u(a.WN * 128u)) + lane;           // logit of spin 128g+j: lt[32 j]
-  long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + 128u * 128u) + lane;  // [m]
+  // logit of spin i of the current group: lt[loff + 32 (i & 127)] (with producers, successive
+  // groups alternate between two buffers, loff = 0 or 4096)
+  float *lt = reinterpret_cast<float *>(wbase + align16u(a.WN * 128u)) + lane;
+  long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + lbytes) + lane;  // [m]
+
+  if (producer) {
+    // The consumer takes the groups g = 0 .. NG-1 of every sweep t of every iteration k in order
+    // (fill f = running index): buffer f & 1, full[f & 1] completes its (f >> 1)-th phase when
+    // filled, empty[f & 1] when the consumer has moved past it.
+    const uint2 pkey = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+    const uint32_t psrho = ((uint32_t)s << 20) | (uint32_t)rho;
+    const int NG = (N + 127) >> 7;
+    uint32_t f = 0;
+    for (int k = 0; k < a.K; ++k)
+      for (int t = 0; t < a.T; ++t)
+        for (int g = 0; g < NG; ++g, ++f) {
+          const uint32_t b = f & 1u;
+          if (f >= 2) mbar_wait(mb + 2 + b, ((f >> 1) - 1u) & 1u);
+          float *dst = lt + 32 * 128 * b;
+          const int nw = min(4, (N - 128 * g + 31) >> 5);
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const uint4 w4 = philox_group(pkey, g, j, t, k, psrho);
+            dst[32 * (j + 0)] = logit_signed(w4.x);
+            if (nw > 1) dst[32 * (j + 32)] = logit_signed(w4.y);
+            if (nw > 2) dst[32 * (j + 64)] = logit_signed(w4.z);
+            if (nw > 3) dst[32 * (j + 96)] = logit_signed(w4.w);
+          }
+          mbar_arrive(mb + b);
+        }
+    return;
+  }
 
   const double c_o = Hp->c_o, c_p = Hp->c_p, c_l = Hp->c_l;
   const float twocp = (float)(2.0 * c_p), cpf = (float)c_p;
@@ -104,6 +168,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
   const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
   const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
   const int Wn = (n + 31) >> 5;
+  uint32_t pf = 0;                                     // groups taken from the producer so far
+  int loff = 0;                                        // buffer of the current group (0 without producers)
 
   for (int k = 0; k < a.K; ++k) {
     // ---- per-iteration constants: c_l Lambda_m (rounded once), error-bound slope E1 ----
@@ -140,11 +206,18 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         }
       };
       auto fill_group = [&](int g) {
-        const int nw = min(4, (N - 128 * g + 31) >> 5);
-        if (nw >= 4) fill_words(g, std::integral_constant<int, 4>{});
-        else if (nw == 3) fill_words(g, std::integral_constant<int, 3>{});
-        else if (nw == 2) fill_words(g, std::integral_constant<int, 2>{});
-        else fill_words(g, std::integral_constant<int, 1>{});
+        if (prod) {                                        // the producer's buffer (g & 1)
+          if (pf >= 1) mbar_arrive(mb + 2 + ((pf - 1u) & 1u));   // done with the previous group
+          mbar_wait(mb + (pf & 1u), (pf >> 1) & 1u);
+          loff = (int)(pf & 1u) * (32 * 128);
+          ++pf;
+        } else {
+          const int nw = min(4, (N - 128 * g + 31) >> 5);
+          if (nw >= 4) fill_words(g, std::integral_constant<int, 4>{});
+          else if (nw == 3) fill_words(g, std::integral_constant<int, 3>{});
+          else if (nw == 2) fill_words(g, std::integral_constant<int, 2>{});
+          else fill_words(g, std::integral_constant<int, 1>{});
+        }
         c_philox += 32;
       };
       // Certified decision [u < sigma(z)] (R18, R19) from z, its error bound e and l = logit(u)
@@ -198,12 +271,12 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         if ((w & 3) == 0) fill_group(w >> 2);
         const int iend = min(32, n - 32 * w);
         // state-independent operands of the current step, prefetched one step ahead
-        float l = lt[32 * ((32 * w) & 127)];
+        float l = lt[loff + 32 * ((32 * w) & 127)];
         float4 ic = sIc[32 * w];                          // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
         float G_n = sBand[32 * w + 1];
         for (int ii = 0; ii < iend; ++ii) {
           const int i = 32 * w + ii;
-          const float l_n = lt[32 * ((i + 1) & 127)];     // valid for ii + 1 < iend (same group)
+          const float l_n = lt[loff + 32 * ((i + 1) & 127)];     // valid for ii + 1 < iend (same group)
           const float4 ic_n = sIc[i + 1];                 // padded entry n
           const float G_nn = sBand[i + 2 <= n ? i + 2 : n];
           const int xb = (xcur >> ii) & 1u;
@@ -254,7 +327,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         for (int q = 0; q < qm; ++q, ++i) {
           if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
           if ((i & 127) == 0) fill_group(i >> 7);
-          const float l = lt[32 * (i & 127)];
+          const float l = lt[loff + 32 * (i & 127)];
           const int xb = (xcur >> (i & 31)) & 1u;
           const float A = (float)(1u << q);
           const float sg = xb ? -1.0f : 1.0f;
@@ -393,15 +466,22 @@ typedef void (*mkp_kernel_t)(const RunArgs);
 
 static int mm_for(int M) { return M <= 4 ? 4 : (M <= 8 ? 8 : (M <= 16 ? 16 : (M <= 32 ? 32 : -1))); }
 
-static mkp_kernel_t mkp_kernel_for(int MM, int M) {
-  if (MM == 8 && M == 5) return saim_mkp_kernel<8, 5>;
-  if (MM == 16 && M == 10) return saim_mkp_kernel<16, 10>;
-  if (MM == 32 && M == 30) return saim_mkp_kernel<32, 30>;
+// Producer-warp instantiations exist for M <= 8 (where one consumer warp per SMSP is the norm).
+static mkp_kernel_t mkp_kernel_for(int MM, int M, bool prod = false) {
+  if (prod) {
+    if (MM == 8 && M == 5) return saim_mkp_kernel<8, 5, true>;
+    if (MM == 4) return saim_mkp_kernel<4, 4, true>;
+    if (MM == 8) return saim_mkp_kernel<8, 8, true>;
+    return nullptr;
+  }
+  if (MM == 8 && M == 5) return saim_mkp_kernel<8, 5, false>;
+  if (MM == 16 && M == 10) return saim_mkp_kernel<16, 10, false>;
+  if (MM == 32 && M == 30) return saim_mkp_kernel<32, 30, false>;
   switch (MM) {
-    case 4: return saim_mkp_kernel<4, 4>;
-    case 8: return saim_mkp_kernel<8, 8>;
-    case 16: return saim_mkp_kernel<16, 16>;
-    case 32: return saim_mkp_kernel<32, 32>;
+    case 4: return saim_mkp_kernel<4, 4, false>;
+    case 8: return saim_mkp_kernel<8, 8, false>;
+    case 16: return saim_mkp_kernel<16, 16, false>;
+    case 32: return saim_mkp_kernel<32, 32, false>;
     default: return nullptr;
   }
 }
@@ -409,7 +489,7 @@ static mkp_kernel_t mkp_kernel_for(int MM, int M) {
 // Plan the MKP launch: padded constraint count MM, blob layout, per-warp bytes and the maximum
 // warps per CTA allowed by threads/registers and shared memory.  Returns 0 or -1 (does not fit).
 int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
-             int *max_wpc) {
+             int *max_wpc, uint32_t *per_warp_prod, int *max_wpc_prod) {
   const int MM = mm_for(M);
   if (MM < 0) return -1;
   mkp_kernel_t k = mkp_kernel_for(MM, M);
@@ -424,6 +504,19 @@ int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blo
   if (wpc < 1) return -1;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(L.bytes + wpc * pw)) != cudaSuccess)
     return -1;
+  // with producer warps (M <= 8): 2 warps per consumer, larger per-consumer region
+  *per_warp_prod = mkp_warp_bytes(WN, MM, 1);
+  *max_wpc_prod = 0;
+  mkp_kernel_t kp = mkp_kernel_for(MM, M, true);
+  cudaFuncAttributes attrp;
+  if (kp && cudaFuncGetAttributes(&attrp, kp) == cudaSuccess) {
+    int wpcp = attrp.maxThreadsPerBlock / 64;
+    const long long by_smem_p = ((long long)smem_optin - L.bytes - attrp.sharedSizeBytes - 64) / *per_warp_prod;
+    if (by_smem_p < wpcp) wpcp = (int)by_smem_p;
+    if (wpcp >= 1 && cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(L.bytes + wpcp * *per_warp_prod)) == cudaSuccess)
+      *max_wpc_prod = wpcp;
+  }
   *MM_out = MM;
   *blob_bytes = L.bytes;
   *per_warp = pw;
@@ -431,12 +524,14 @@ int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blo
   return 0;
 }
 
+// wpc consumer warps per CTA (plus as many producer warps if a.mkp_prod; per_warp is then the
+// producer-mode per-consumer region).
 cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st) {
-  mkp_kernel_t k = mkp_kernel_for(MM, a.M);
+  mkp_kernel_t k = mkp_kernel_for(MM, a.M, a.mkp_prod != 0);
   if (!k) return cudaErrorInvalidValue;
   const int warps_per_inst = (a.R + 31) / 32;
   dim3 grid((warps_per_inst + wpc - 1) / wpc, n_inst);
-  k<<<grid, wpc * 32, a.blob_bytes + wpc * per_warp, st>>>(a);
+  k<<<grid, wpc * 32 * (a.mkp_prod ? 2 : 1), a.blob_bytes + wpc * per_warp, st>>>(a);
   return cudaGetLastError();
 }
 

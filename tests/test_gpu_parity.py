@@ -249,7 +249,8 @@ def _mkp(n, m, t, seed):
 
 # MKP kernel variants: default (outcome tree L = 2 for M <= 8, lockstep for M > 8), lockstep,
 # outcome tree with L = 2 and 4, row split over 2 lanes (honoured for M > 8; else the default)
-MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("tree_L2", 4), ("tree_L4", 8), ("split2", 16)]
+MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("lockstep_noprod", 2 | 64), ("tree_L2", 4), ("tree_L4", 8),
+                ("split2", 16)]
 
 
 @pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
@@ -261,7 +262,7 @@ def test_mkp_parity_small(P, n, m, variant):
     g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=40, K=4, T=30, flags=variant)
     assert g["info"]["kernel"] == 2
     default = 2 if m <= 8 else 1
-    want = {0: default, 2: 1, 4: 2, 8: 4, 16: 2}[variant]
+    want = {0: default, 2: 1, 66: 1, 4: 2, 8: 4, 16: 2}[variant]
     assert g["info"]["lanes_per_replica"] == want
 
 
