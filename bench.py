@@ -293,6 +293,9 @@ def main():
     sm_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     peak_ops = sm_count * LANES_PER_SM_CLK * sm_mhz * 1e6
     achieved = ops / t_step
+    # SURVEY.md 8(d) transparency variant: the same time priced as if every decision drew its
+    # uniform (f_u = 1) -- the model of a sampler without saturation certificates
+    ops_rng_all = (evaluated * (OPS_DECISION + OPS_UNIFORM) + c0["flips"] * OPS_FLIP_PER_ITEM * n_items)
 
     # ---- end-to-end through the public API with host buffers (create from host arrays = H2D,
     # run, D2H of the results), timed on the device stream with a host sync at the end ----
@@ -339,7 +342,12 @@ def main():
                          "ops_per_launch": ops, "ops_model": f"{OPS_DECISION}*evaluated decisions + {OPS_UNIFORM}*uniforms + "
                                                             f"{OPS_FLIP_PER_ITEM}*n*flips (lane-ops)",
                          "peak_basis": f"{sm_count} SMs x {LANES_PER_SM_CLK} lanes/clk x {sm_mhz:.0f} MHz "
-                                       "(measured median SM clock under load)"},
+                                       "(measured median SM clock under load)",
+                         "rng_every_update": {"achieved": ops_rng_all / t_step / 1e12,
+                                              "frac": ops_rng_all / t_step / peak_ops,
+                                              "ops_model": "f_u = 1: every evaluated decision priced with a uniform"},
+                         "ncu": "profiles/r01/qkp_config2_K200_raw_selected.csv (issue slots, pipes, "
+                                "shared-memory wavefronts, DRAM bytes)"},
             "counters": c0,
             "evaluated_sweep_fraction": c0["sweeps"] / float(R * cfg.K * cfg.T * sol.n_inst),
             "no_freeze_exit": nofreeze,
