@@ -333,7 +333,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // bounds |z_f32 - z| for every reachable state (phi_bound, v_bound; 4x margin over 3*2^-24).
       const float B0 = fmaf(tf, ws->e0s, kSatThr), B1 = tf * ws->e1s;
       int g = 0;                                          // current 128-spin group (4 blocks)
-      bool have_u = false;                                // group g's words drawn (ws->uw)?
 
       // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
       // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
@@ -361,12 +360,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           const uint32_t need = __ballot_sync(kFull, mine && !sat);
           if (need) {
             if (!have_l) {
-              if (!have_u) {
-                const uint4 u4 = philox_group_lazy(ws->key, g, lane, t, k, ws->srho);
-                ws->uw[0][lane] = u4.x; ws->uw[1][lane] = u4.y; ws->uw[2][lane] = u4.z; ws->uw[3][lane] = u4.w;
-                have_u = true;
-                nphil += 32u;
-              }
               w = ws->uw[bb][lane];
               l = logit_f32(w);
               el = kLogitAbs + kLogitRel * fabsf(l);
@@ -440,7 +433,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         g = (__ffs(todo) - 1) >> 2;
         const uint32_t gb = (todo >> (4 * g)) & 15u;        // blocks of group g to scan
         todo &= ~(15u << (4 * g));
-        have_u = false;
         uint32_t nq = 0;
 #pragma unroll
         for (int bb = 0; bb < 4; ++bb)
@@ -451,6 +443,11 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #endif
         if (gb & ~m) certify((gb & ~m) << (4 * g));        // scanned and quiet: certified
         if (m) {
+          // the group's uniform words, drawn once per visit of a group with a non-quiet block
+          const uint4 u4 = philox_group_lazy(ws->key, g, lane, t, k, ws->srho);
+          ws->uw[0][lane] = u4.x; ws->uw[1][lane] = u4.y; ws->uw[2][lane] = u4.z; ws->uw[3][lane] = u4.w;
+          __syncwarp();
+          nphil += 32u;
           const uint32_t nf0 = nflip;
           handle_group(m);
           if (nflip != nf0) {
