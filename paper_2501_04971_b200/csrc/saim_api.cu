@@ -226,10 +226,13 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     const int E = 4 / ctx->qb;
     const int QW = (ctx->npl + E - 1) / E;
     const int NBP = ((ctx->npl + 2) + 3) & ~3;            // blocks incl. padding to a 4-block group
+    // [A_ext | c | Q rows]: offsets fixed by the (NPL, QB) template, so the kernel addresses all
+    // three from one register (saim_layout.h)
     const uint32_t q_bytes = align16((uint32_t)n * QW * 128u);
-    ctx->a_off = q_bytes;
-    ctx->c_off = ctx->a_off + align16(NBP * 32 * 4);
-    ctx->blob_bytes = ctx->c_off + align16(ctx->npl * 32 * 4);
+    ctx->a_off = 0;
+    ctx->c_off = align16(NBP * 32 * 4);
+    ctx->x_off = ctx->c_off + align16(ctx->npl * 32 * 4);   // Q rows
+    ctx->blob_bytes = ctx->x_off + q_bytes;
     if ((int)ctx->blob_bytes + 64 > smem_optin) {
       delete ctx;
       return fail(SAIM_ESMEM, "QKP blob of %u bytes exceeds shared memory (%d)", ctx->blob_bytes, smem_optin);
@@ -241,7 +244,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
       unsigned char *B = blob.data() + (size_t)s * ctx->blob_bytes;
       const int32_t *Q = prob->Q ? prob->Q + (size_t)s * n * n : nullptr;
       for (int j = 0; j < n; ++j) {
-        uint32_t *row = reinterpret_cast<uint32_t *>(B + (size_t)j * QW * 128u);
+        uint32_t *row = reinterpret_cast<uint32_t *>(B + ctx->x_off + (size_t)j * QW * 128u);
         for (int w = 0; w < QW; ++w)
           for (int l = 0; l < 32; ++l) {
             uint32_t word = 0;

@@ -4,12 +4,15 @@
 // stages into shared memory with a single TMA bulk copy (cp.async.bulk):
 //
 //   QKP kernel (M <= 1, quadratic objective):
+//     [A_ext]                float[NBP*32]: item weights, then slack weights 1,2,..,2^(q-1), then
+//                            NaN (no spin).
+//     [c]                    int32[NPL*32]: objective linear term per item, 0 beyond n.
 //     [Q rows, lane-major]   n rows x QW words x 32 lanes x 4 B.  Word w of lane l in row j packs
 //                            the entries Q[j][32*(E*w+e) + l] (e = 0..E-1, E = 4/qbytes) as
 //                            unsigned (Q + 2^(8*qbytes-1)); entries of non-existent items are the
 //                            code of 0.  A flip of item j streams one row: lane l reads QW words.
-//     [A_ext]                float[NB*32]: item weights, then slack weights 1,2,..,2^(q-1), then 0.
-//     [c]                    int32[NPL*32]: objective linear term per item, 0 beyond n.
+//     (A_ext and c first: their sizes depend only on the kernel's (NPL, QB) instantiation, so all
+//     three arrays sit at compile-time offsets from one base.)
 //   MKP kernel (linear objective, M <= 32):
 //     [Acol]                 int16 x M x n_pad (item columns A[.][i]), stored [i][M] so one spin's
 //                            column is contiguous.

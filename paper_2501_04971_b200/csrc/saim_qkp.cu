@@ -137,9 +137,11 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const int ridx = blockIdx.x * (blockDim.x >> 5) + warp;
   if (ridx >= a.R) return;
   const InstHdr *Hp = a.hdr + s;
-  const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem) + lane;       // Q word (row 0, w 0) of this lane
-  const float *sAl = reinterpret_cast<const float *>(smem + a.a_off) + lane;   // A_ext[32b + lane] (NaN-padded)
-  const int32_t *sC = reinterpret_cast<const int32_t *>(smem + a.c_off);
+  // blob layout [A_ext | c | Q rows] (saim_layout.h): compile-time offsets from one base
+  constexpr uint32_t kCOff = (NBP * 32 * 4 + 15) & ~15u, kQOff = kCOff + ((NPL * 32 * 4 + 15) & ~15u);
+  const float *sAl = reinterpret_cast<const float *>(smem) + lane;              // A_ext[32b + lane] (NaN-padded)
+  const int32_t *sC = reinterpret_cast<const int32_t *>(smem + kCOff);
+  const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem + kQOff) + lane;  // Q word (row 0, w 0) of this lane
   unsigned char *wbase = smem + a.blob_bytes + warp * qkp_warp_smem_bytes<NPL>();
   float *phs = reinterpret_cast<float *>(wbase) + lane;                        // (2x_i - 1) phi_i, i = 32b + lane
   float *asg = reinterpret_cast<float *>(wbase) + NBP * 32 + lane;             // (2x_i - 1) A_i
