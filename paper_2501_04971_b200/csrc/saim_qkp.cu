@@ -278,10 +278,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         const int b = __ffs(allb & ~qmask) - 1;
         const int bb = b & 3, gq = b >> 2;
         const float A = sAl[32 * b];
-        const bool xb = (xm >> b) & 1u;
-        const float sg = xb ? -1.0f : 1.0f;
-        const float phib = -sg * phs[32 * b];
-        const float v = fmaf(A, sg, r2);
+        bool xb = (xm >> b) & 1u;
+        float sg = xb ? -1.0f : 1.0f;
+        const float phib = -sg * phs[32 * b];             // phi: constant (items do not flip here)
+        float v = fmaf(A, sg, r2);
         const bool mine = lane < N - 32 * b;
         const float k1s = ws->k1s, k2s = ws->k2s, k3s = ws->k3s;
         uint32_t wreg = 0, pmask = 0;
@@ -322,8 +322,49 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
               if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
             }
           }
-          if (__ballot_sync(kFull, mine && nx != (int)xb)) break;   // a flip: general path
-          nunif += __popc(need);
+          const uint32_t fm = __ballot_sync(kFull, mine && nx != (int)xb);
+          uint32_t drew = need;
+          if (fm) {
+            // A single slack flip (lane L) that keeps 2r inside the certificates' window and after
+            // which the later lanes of b flip nothing is completed here; anything else (an item
+            // flip, a second flip, the window left) leaves the whole sweep to the general path.
+            const int L = __ffs(fm) - 1;
+            const float dl = __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f;
+            const float r2n = fmaf(dl + dl, __shfl_sync(kFull, A, L), r2);
+            if (32 * b + L < n || fabsf(r2n - r2c) > a.rtol2) break;
+            const float v2 = fmaf(A, sg, r2n);
+            const float z2 = fmaf(K1, phib, -fmaf(AK2, v2, AK3));
+            const float S2 = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v2), fabsf(AK3)));
+            const bool mine2 = mine && lane > L;
+            const bool sat2 = fabsf(z2) * kZScale - S2 > kSatThr20;
+            int nx2 = z2 > 0.0f;
+            const uint32_t need2 = __ballot_sync(kFull, mine2 && !sat2);
+            if (need2 & ~pmask) break;                    // (words not at hand: general path)
+            if (mine2 && !sat2) {
+              const float d = z2 - l;
+              if (fabsf(d) > (S2 * (1.0f / kZScale) + el) * 1.0001f) {
+                nx2 = d > 0.0f;
+              } else {
+                const int rs = decide_fp64(phib, v2, A, t, Hp, ws, w);
+                nx2 = rs & 1;
+                atomicAdd(&ws->cnt[kCntFp64], 1u);
+                if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
+              }
+            }
+            if (__ballot_sync(kFull, mine2 && nx2 != (int)xb)) break;
+            r2 = r2n;                                     // apply the slack flip: r += delta A_L
+            if (lane == L) {
+              xm ^= (1u << b);
+              phs[32 * b] = -phs[32 * b];
+              asg[32 * b] = -asg[32 * b];
+              xb = !xb;
+              sg = -sg;
+            }
+            v = fmaf(A, sg, r2);
+            ++nflip;
+            drew |= need2;
+          }
+          nunif += __popc(drew);
         }
         if (t >= a.T) break;
       }
