@@ -122,6 +122,8 @@ typedef struct {
   int32_t smem_bytes;      /* dynamic shared memory per CTA */
   int32_t q_bytes;         /* bytes per stored Q entry (1 or 2), 0 if no Q */
   int32_t lanes_per_replica;
+  int32_t phi_packed;      /* QKP: 1 if phi is held as biased int16 pairs (int8 Q and |phi| <= 32767
+                            * in every state, host-proven), 0 = fp32 phi */
 } saim_info;
 
 typedef struct saim_ctx saim_ctx;

@@ -57,7 +57,7 @@ class _Outputs(C.Structure):
 class _Info(C.Structure):
     _fields_ = [(f, C.c_int32) for f in ["n_inst", "n_items", "n_cons", "n_spins_max", "words_items",
                                          "words_full", "kernel", "smem_bytes", "q_bytes",
-                                         "lanes_per_replica"]]
+                                         "lanes_per_replica", "phi_packed"]]
 
 
 _lib = None

@@ -21,8 +21,8 @@
 
 namespace saim {
 int qkp_npl_bucket(int npl);
-cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *max_wpc);
-cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st);
+cudaError_t qkp_configure(int npl, int qb, int pk, int blob_bytes, int smem_optin, int *max_wpc);
+cudaError_t qkp_launch(int npl, int qb, int pk, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st);
 int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
              int *max_wpc, uint32_t *per_warp_prod, int *max_wpc_prod);
 cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
@@ -55,7 +55,7 @@ struct saim_ctx {
   int device = 0;
   int n_inst = 0, n = 0, M = 0;
   int kernel = 0;       // 1 = QKP, 2 = MKP
-  int npl = 0, qb = 0;  // QKP
+  int npl = 0, qb = 0, pk = 0;  // QKP (pk: phi packed as two int16 per word)
   int lanes = 32;       // lanes per replica (QKP: 32; MKP: 1 lockstep, L = 2 or 4 outcome tree)
   int mm = 0;           // MKP padded constraint count
   int mkp_kind = 0;     // MKP kernel: 0 lockstep, 1 outcome tree, 2 row split
@@ -120,6 +120,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
 
   // ---- per-instance validation, slack, scales, range proofs ----
   long long rmax_all = 0;
+  long long phib_all = 0;   // max phi bound over instances (QKP packed-phi eligibility)
   int qmax_abs = 0;
   for (int s = 0; s < S; ++s) {
     const int32_t *Q = prob->Q ? prob->Q + (size_t)s * n * n : nullptr;
@@ -177,6 +178,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     h.c_p = P / ((double)sc * (double)sc);
     h.c_l = par->eta / ((double)sc * (double)sc);
     h.phi_bound = (double)phi_bound;
+    phib_all = std::max(phib_all, phi_bound);
     {
       long long amax = 0;
       for (int k = 0; k < M; ++k) {
@@ -223,6 +225,9 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     if (ctx->npl < 0) { delete ctx; return fail(SAIM_ESMEM, "n = %d items > 512 (Q does not fit shared memory)", n); }
     ctx->qb = qmax_abs <= 127 ? 1 : (qmax_abs <= 32767 ? 2 : 0);
     if (!ctx->qb) { delete ctx; return fail(SAIM_ERANGE, "|Q| entries > 32767 need wider storage"); }
+    // int8 Q with |phi| <= 32767 in every state: phi held as biased int16 pairs, a Q-row update is
+    // one packed integer add per two items (DESIGN.md 6.1 "Packed phi")
+    ctx->pk = (ctx->qb == 1 && phib_all <= 32767) ? 1 : 0;
     const int E = 4 / ctx->qb;
     const int QW = (ctx->npl + E - 1) / E;
     const int NBP = ((ctx->npl + 2) + 3) & ~3;            // blocks incl. padding to a 4-block group
@@ -268,7 +273,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
       int32_t *cc = reinterpret_cast<int32_t *>(B + ctx->c_off);
       for (int i = 0; i < n; ++i) cc[i] = prob->c[(size_t)s * n + i];
     }
-    e = qkp_configure(ctx->npl, ctx->qb, ctx->smem_bytes, smem_optin, &ctx->max_wpc);
+    e = qkp_configure(ctx->npl, ctx->qb, ctx->pk, ctx->smem_bytes, smem_optin, &ctx->max_wpc);
     if (e == cudaErrorInvalidConfiguration) {
       delete ctx;
       return fail(SAIM_ESMEM, "QKP layout (%u bytes) leaves no room for one warp's state in shared memory", ctx->blob_bytes);
@@ -417,7 +422,7 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     const long long warps = (long long)R * ctx->n_inst;
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
-    e = qkp_launch(ctx->npl, ctx->qb, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
+    e = qkp_launch(ctx->npl, ctx->qb, ctx->pk, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
   } else if (ctx->mkp_kind == 0) {
     const long long warps = (long long)((R + 31) / 32) * ctx->n_inst;   // 32 replicas per warp (lockstep)
     int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
@@ -449,6 +454,7 @@ extern "C" int saim_get_info(const saim_ctx *ctx, saim_info *out) {
   out->kernel = ctx->kernel;
   out->smem_bytes = ctx->smem_bytes;
   out->q_bytes = ctx->kernel == 1 ? ctx->qb : 0;
+  out->phi_packed = ctx->kernel == 1 ? ctx->pk : 0;
   out->lanes_per_replica = ctx->lanes;
   return SAIM_OK;
 }

@@ -121,7 +121,11 @@ __host__ __device__ constexpr int qkp_warp_smem_bytes() {
 
 // Shared memory: [instance blob: Q rows | A_ext (NaN-padded) | c]
 //                [per warp: phs = (2x-1) phi | asg = (2x-1) A, each NBP*32 floats | WarpState]
-template <int NPL, int QB>
+// PK (packed phi, int8 Q with |phi| <= 32767 in every state, host-proven): the phs region holds
+// instead phw[p][lane] = (phi_{32(2p)+lane} + 2^15) | (phi_{32(2p+1)+lane} + 2^15) << 16, the
+// unsigned phi of two blocks per word.  A Q-row update is then one packed integer add per two
+// items: both 16-bit halves stay in [1, 65535], so no carry crosses between them.
+template <int NPL, int QB, bool PK>
 __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunArgs a) {
   constexpr int E = 4 / QB;                          // Q entries per 32-bit word
   constexpr int QW = (NPL + E - 1) / E;              // words per lane per Q row
@@ -144,6 +148,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem + kQOff) + lane;  // Q word (row 0, w 0) of this lane
   unsigned char *wbase = smem + a.blob_bytes + warp * qkp_warp_smem_bytes<NPL>();
   float *phs = reinterpret_cast<float *>(wbase) + lane;                        // (2x_i - 1) phi_i, i = 32b + lane
+  uint32_t *phw = reinterpret_cast<uint32_t *>(wbase) + lane;                  // PK: packed phi pairs
   float *asg = reinterpret_cast<float *>(wbase) + NBP * 32 + lane;             // (2x_i - 1) A_i
   WarpState *ws = reinterpret_cast<WarpState *>(wbase + 2 * NBP * 32 * 4);
   const int n = a.n;
@@ -156,9 +161,19 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   // x = 0: phi_i = -c_i, so (2x-1) phi = c_i; (2x-1) A = -A.
 #pragma unroll
   for (int m = 0; m < NBP; ++m) {
-    phs[32 * m] = (32 * m + lane < n) ? (float)sC[32 * m + lane] : 0.0f;
+    if constexpr (PK) {
+      const uint32_t h = 32768u - (uint32_t)((32 * m + lane < n) ? sC[32 * m + lane] : 0);
+      if (m & 1) phw[32 * (m >> 1)] |= h << 16; else phw[32 * (m >> 1)] = h;
+    } else {
+      phs[32 * m] = (32 * m + lane < n) ? (float)sC[32 * m + lane] : 0.0f;
+    }
     asg[32 * m] = -sAl[32 * m];
   }
+  // phi_i of this lane's spin in block b (PK: exact via the 2^23 magic-number conversion)
+  auto phi_pk = [&](int b) -> float {
+    return __uint_as_float(__byte_perm(phw[32 * (b >> 1)], 0x4B000000u, (b & 1) ? 0x7632u : 0x7610u)) -
+           (8388608.0f + 32768.0f);
+  };
   if (lane == 0) {
     const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
     ws->bstep = bstep;
@@ -200,13 +215,38 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     r2 = fmaf(dl + dl, AL, r2);
     if (lane == L) {
       xm ^= (1u << b);
-      phs[32 * b] = -phs[32 * b];
+      if constexpr (!PK) phs[32 * b] = -phs[32 * b];
       asg[32 * b] = -asg[32 * b];
     }
     const int j = 32 * b + L;
     if (j < n) {                                    // an item flip moves phi: certificates void
       qmask = 0u;
       const uint32_t *row = sQl + j * (QW * 32);
+      if constexpr (PK) {
+        // phi_i -= delta Q_ij on two items per word: pq = biased bytes (Q + 128) of entries
+        // (2p, 2p+1) as 16-bit halves, phi - delta (pq - 0x00800080)
+        if (dl > 0.0f) {
+#pragma unroll
+          for (int w = 0; w < QW; ++w) {
+            const uint32_t word = row[32 * w];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (4 * w + 2 * h < NPL)
+                phw[32 * (2 * w + h)] = phw[32 * (2 * w + h)] - __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) + 0x00800080u;
+          }
+        } else {
+#pragma unroll
+          for (int w = 0; w < QW; ++w) {
+            const uint32_t word = row[32 * w];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (4 * w + 2 * h < NPL)
+                phw[32 * (2 * w + h)] = phw[32 * (2 * w + h)] + __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) - 0x00800080u;
+          }
+        }
+        ++nflip;
+        return;
+      }
 #pragma unroll
       for (int w = 0; w < QW; ++w) {
         const uint32_t word = row[32 * w];
@@ -280,7 +320,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         const float A = sAl[32 * b];
         bool xb = (xm >> b) & 1u;
         float sg = xb ? -1.0f : 1.0f;
-        const float phib = -sg * phs[32 * b];             // phi: constant (items do not flip here)
+        const float phib = PK ? phi_pk(b) : -sg * phs[32 * b];   // phi: constant (items do not flip here)
         float v = fmaf(A, sg, r2);
         const bool mine = lane < N - 32 * b;
         const float k1s = ws->k1s, k2s = ws->k2s, k3s = ws->k3s;
@@ -355,7 +395,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             r2 = r2n;                                     // apply the slack flip: r += delta A_L
             if (lane == L) {
               xm ^= (1u << b);
-              phs[32 * b] = -phs[32 * b];
+              if constexpr (!PK) phs[32 * b] = -phs[32 * b];
               asg[32 * b] = -asg[32 * b];
               xb = !xb;
               sg = -sg;
@@ -393,7 +433,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         uint32_t drew = 0;                                // lanes that needed their uniform in this visit
         int lo = 0;                                       // lanes in [lo, hi) are still pending
         for (;;) {
-          const float phib = -sg * phs[32 * b];           // phi_i
+          const float phib = PK ? phi_pk(b) : -sg * phs[32 * b];   // phi_i
           const float v = fmaf(A, sg, r2);                // 2 r0 + A
           const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));            // beta_t F_i (fp32)
           const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
@@ -439,7 +479,9 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       //   quiet <=> zz > B0 + B1 |A|;  NaN padding (spins >= N) compares false -> quiet.
       auto scan_one = [&](uint32_t &nq, int b, int bb) {
         const float as = asg[32 * b];
-        const float ph = phs[32 * b];
+        // (2x-1) phi: PK flips phi's sign bit with that of (2x-1) A (signed zero when A = 0)
+        const float ph = PK ? __uint_as_float(__float_as_uint(phi_pk(b)) ^ (__float_as_uint(as) & 0x80000000u))
+                            : phs[32 * b];
         const float v = r2 - as;
         const float tq = fmaf(K2, v, K3);
         const float zz = fmaf(K1, ph, -(as * tq));
@@ -521,7 +563,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 #pragma unroll
     for (int m = 0; m < NPL; ++m) {
       if (((xm >> m) & 1u) && 32 * m + lane < n) {
-        fpart += sC[32 * m + lane] - (int)phs[32 * m];      // x_i (c_i - phi_i); phs = phi when x_i = 1
+        fpart += sC[32 * m + lane] - (int)(PK ? phi_pk(m) : phs[32 * m]);   // x_i (c_i - phi_i); phs = phi when x_i = 1
         load += (int)sAl[32 * m];
       }
     }
@@ -608,12 +650,12 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 // Launch: grid (ceil(R / wpc), n_inst), wpc warps per CTA.
 typedef void (*qkp_kernel_t)(const RunArgs);
 
-template <int NPL, int QB>
-static qkp_kernel_t pick() { return saim_qkp_kernel<NPL, QB>; }
+template <int NPL, int QB, bool PK>
+static qkp_kernel_t pick() { return saim_qkp_kernel<NPL, QB, PK>; }
 
-static qkp_kernel_t qkp_kernel_for(int npl, int qb) {
+static qkp_kernel_t qkp_kernel_for(int npl, int qb, int pk) {
 #define SAIM_QKP_CASE(P)                                \
-  if (npl <= P) return qb == 1 ? pick<P, 1>() : pick<P, 2>();
+  if (npl <= P) return qb == 1 ? (pk ? pick<P, 1, true>() : pick<P, 1, false>()) : pick<P, 2, false>();
   SAIM_QKP_CASE(1) SAIM_QKP_CASE(2) SAIM_QKP_CASE(3) SAIM_QKP_CASE(4) SAIM_QKP_CASE(6)
   SAIM_QKP_CASE(8) SAIM_QKP_CASE(10) SAIM_QKP_CASE(12) SAIM_QKP_CASE(16)
 #undef SAIM_QKP_CASE
@@ -639,8 +681,8 @@ int qkp_npl_bucket(int npl) {
 
 // max_wpc: warps per CTA limited by threads (launch bounds), registers and shared memory
 // (blob + per-warp phi).  Sets the kernel's dynamic shared-memory limit accordingly.
-cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *max_wpc) {
-  qkp_kernel_t k = qkp_kernel_for(npl, qb);
+cudaError_t qkp_configure(int npl, int qb, int pk, int blob_bytes, int smem_optin, int *max_wpc) {
+  qkp_kernel_t k = qkp_kernel_for(npl, qb, pk);
   if (!k) return cudaErrorInvalidValue;
   cudaFuncAttributes attr;
   cudaError_t e = cudaFuncGetAttributes(&attr, k);
@@ -658,8 +700,8 @@ cudaError_t qkp_configure(int npl, int qb, int blob_bytes, int smem_optin, int *
 }
 
 // Dynamic shared memory = blob + wpc * per-warp region (phi + WarpState).
-cudaError_t qkp_launch(int npl, int qb, const RunArgs &a, int n_inst, int wpc, int blob_bytes, cudaStream_t st) {
-  qkp_kernel_t k = qkp_kernel_for(npl, qb);
+cudaError_t qkp_launch(int npl, int qb, int pk, const RunArgs &a, int n_inst, int wpc, int blob_bytes, cudaStream_t st) {
+  qkp_kernel_t k = qkp_kernel_for(npl, qb, pk);
   if (!k) return cudaErrorInvalidValue;
   dim3 grid((a.R + wpc - 1) / wpc, n_inst);
   k<<<grid, wpc * 32, blob_bytes + wpc * qkp_warp_bytes(npl), st>>>(a);

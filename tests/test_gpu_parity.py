@@ -166,7 +166,13 @@ def test_parity_edge_cases(P):
     # Q entries beyond int8 -> int16 shared-memory storage
     p = _qkp(45, 0.5, 6)
     p.Q = (p.Q * 300).astype(np.int32)
-    run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=8, R=8, K=4, T=40)
+    g = run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=8, R=8, K=4, T=40)
+    assert (g["info"]["q_bytes"], g["info"]["phi_packed"]) == (2, 0)
+    # int8 Q whose |phi| bound exceeds int16 (299 x 127): int8 rows with fp32 phi (not packed)
+    p = _qkp(300, 1.0, 13)
+    p.Q = np.where(p.Q != 0, -127, 0).astype(np.int32)
+    g = run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=12, R=8, K=3, T=30)
+    assert (g["info"]["q_bytes"], g["info"]["phi_packed"]) == (1, 0)
     # a high-beta, tiny-field regime (decisions near the sigma boundary exercise the certification)
     p = _qkp(30, 0.5, 7)
     run_both(P, [p], [0.01], 0.001, 0.05, seed=9, R=8, K=4, T=50)
@@ -201,8 +207,9 @@ def test_parity_config2_sampled(P):
     """BASELINE config 2 (headline) at full size; sampled replicas (the first, the last and a
     contiguous block of 48) against the oracle."""
     cfg = si.config_instances(2)
-    run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
-             reps=[0, 4095], block=(1024, 48))
+    g = run_both(P, cfg.instances, cfg.P, cfg.eta, cfg.beta_max, seed=1, R=cfg.R, K=cfg.K, T=cfg.T,
+                 reps=[0, 4095], block=(1024, 48))
+    assert (g["info"]["q_bytes"], g["info"]["phi_packed"]) == (1, 1)
 
 
 @pytest.mark.parametrize("cfg_idx", [0, 1])
