@@ -324,14 +324,18 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         float v = fmaf(A, sg, r2);
         const bool mine = lane < N - 32 * b;
         const float k1s = ws->k1s, k2s = ws->k2s, k3s = ws->k3s;
+        // The fields are constant here, so z = t z1 and S = t S1 with z1, S1 per unit t: 5
+        // roundings of S at most (3 of the fp32 constants and z1, one of t z1), inside the 2^-20 S
+        // bound the decisions below use.
+        const float Ak2 = A * k2s, Ak3 = A * k3s;
+        float z1 = fmaf(k1s, phib, -fmaf(Ak2, v, Ak3));
+        float S1 = fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v), fabsf(Ak3)));
+        float tf = (float)t;                                // exact (t < 2^24)
         uint32_t wreg = 0, pmask = 0;
+        float lreg = 0.0f;                                  // logit of wreg, taken once per refill
         int pt0 = 0, plo = 0, pw = 32, pS = 0;
-        for (; t < a.T; ++t) {
-          const float tf = (float)t;
-          const float K1 = tf * k1s, K2 = tf * k2s, K3 = tf * k3s;
-          const float AK2 = A * K2, AK3 = A * K3;
-          const float z = fmaf(K1, phib, -fmaf(AK2, v, AK3));
-          const float S = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v), fabsf(AK3)));
+        for (; t < a.T; ++t, tf += 1.0f) {
+          const float z = tf * z1, S = tf * S1;
           const bool sat = fabsf(z) * kZScale - S > kSatThr20;
           int nx = z > 0.0f;
           const uint32_t need = __ballot_sync(kFull, mine && !sat);
@@ -343,19 +347,24 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             const int sj = (int)(((float)lane + 0.5f) * __frcp_rn((float)pw));
             const uint4 u4 = philox_group_lazy(ws->key, gq, plo + lane - sj * pw, t + sj, k, ws->srho);
             wreg = sel4(u4, bb);
+            lreg = logit_f32(wreg);
             pt0 = t;
             pS = (int)(32.5f * __frcp_rn((float)pw));
             pmask = (pw == 32) ? kFull : (((1u << pw) - 1u) << plo);
             nphil += 32u;
           }
-          const uint32_t w = __shfl_sync(kFull, wreg, ((t - pt0) * pw + lane - plo) & 31);
-          const float l = logit_f32(w);
+          const int src = ((t - pt0) * pw + lane - plo) & 31;
+          const float l = __shfl_sync(kFull, lreg, src);
           const float el = kLogitAbs + kLogitRel * fabsf(l);
+          bool band = false;                              // inside the fp32 error band: fp64 below
           if (mine && !sat) {
             const float d = z - l;
-            if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
-              nx = d > 0.0f;
-            } else {
+            nx = d > 0.0f;
+            band = !(fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f);
+          }
+          if (__any_sync(kFull, band)) {                  // rare: the raw word for the fp64 path
+            const uint32_t w = __shfl_sync(kFull, wreg, src);
+            if (band) {
               const int rs = decide_fp64(phib, v, A, t, Hp, ws, w);
               nx = rs & 1;
               atomicAdd(&ws->cnt[kCntFp64], 1u);
@@ -373,18 +382,22 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             const float r2n = fmaf(dl + dl, __shfl_sync(kFull, A, L), r2);
             if (32 * b + L < n || fabsf(r2n - r2c) > a.rtol2) break;
             const float v2 = fmaf(A, sg, r2n);
-            const float z2 = fmaf(K1, phib, -fmaf(AK2, v2, AK3));
-            const float S2 = fmaf(K1, fabsf(phib), fmaf(fabsf(AK2), fabsf(v2), fabsf(AK3)));
+            const float z2 = tf * fmaf(k1s, phib, -fmaf(Ak2, v2, Ak3));
+            const float S2 = tf * fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v2), fabsf(Ak3)));
             const bool mine2 = mine && lane > L;
             const bool sat2 = fabsf(z2) * kZScale - S2 > kSatThr20;
             int nx2 = z2 > 0.0f;
             const uint32_t need2 = __ballot_sync(kFull, mine2 && !sat2);
             if (need2 & ~pmask) break;                    // (words not at hand: general path)
+            bool band2 = false;
             if (mine2 && !sat2) {
               const float d = z2 - l;
-              if (fabsf(d) > (S2 * (1.0f / kZScale) + el) * 1.0001f) {
-                nx2 = d > 0.0f;
-              } else {
+              nx2 = d > 0.0f;
+              band2 = !(fabsf(d) > (S2 * (1.0f / kZScale) + el) * 1.0001f);
+            }
+            if (__any_sync(kFull, band2)) {
+              const uint32_t w = __shfl_sync(kFull, wreg, src);
+              if (band2) {
                 const int rs = decide_fp64(phib, v2, A, t, Hp, ws, w);
                 nx2 = rs & 1;
                 atomicAdd(&ws->cnt[kCntFp64], 1u);
@@ -401,6 +414,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
               sg = -sg;
             }
             v = fmaf(A, sg, r2);
+            z1 = fmaf(k1s, phib, -fmaf(Ak2, v, Ak3));
+            S1 = fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v), fabsf(Ak3)));
             ++nflip;
             drew |= need2;
           }
