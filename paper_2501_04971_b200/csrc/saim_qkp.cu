@@ -311,9 +311,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // as long as nothing flips.  While b's own decisions flip nothing, its fields stay constant
       // and a whole sweep is just b's 32 decisions: run such sweeps back to back here.  The sweep
       // in which b would flip a spin (or turns quiet) is left to the general path below, which
-      // re-derives the same decisions from the same state and uniforms.  The uniforms of b's
-      // unsaturated lanes [plo, plo + pw) for the next pS = 32 / pw sweeps come from one
-      // warp-wide Philox call, lane j holding word bb of spin lane plo + j % pw, sweep pt0 + j / pw.
+      // re-derives the same decisions from the same state and uniforms.  Sweeps are evaluated
+      // 32 / pw at a time (pw = width of b's unsaturated lanes), one lane per (spin, sweep).
       if (hot_loop && qmask != allb && !((allb & ~qmask) & ((allb & ~qmask) - 1u))) {
         const int b = __ffs(allb & ~qmask) - 1;
         const int bb = b & 3, gq = b >> 2;
@@ -331,95 +330,112 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         float z1 = fmaf(k1s, phib, -fmaf(Ak2, v, Ak3));
         float S1 = fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v), fabsf(Ak3)));
         float tf = (float)t;                                // exact (t < 2^24)
-        uint32_t wreg = 0, pmask = 0;
-        float lreg = 0.0f;                                  // logit of wreg, taken once per refill
-        int pt0 = 0, plo = 0, pw = 32, pS = 0;
-        for (; t < a.T; ++t, tf += 1.0f) {
+        for (; t < a.T;) {
+          // One step covers sweeps [t, t + pS): on sweep t the saturated lanes of b are certified
+          // for every later sweep too (constant fields, |z| = t |z1| grows with t); the pw lanes
+          // [plo, plo + pw) that are not saturated at t are evaluated for pS = 32 / pw sweeps at
+          // once, lane j taking spin lane sp = plo + j % pw at sweep t + j / pw with its own
+          // Philox word.  All sweeps before the first one with a flip are complete (nothing
+          // changed); that sweep is finished here if its only flip is an in-window slack flip,
+          // else left to the general path.
           const float z = tf * z1, S = tf * S1;
           const bool sat = fabsf(z) * kZScale - S > kSatThr20;
-          int nx = z > 0.0f;
           const uint32_t need = __ballot_sync(kFull, mine && !sat);
-          if (!need) break;                               // b quiet (or flipping): general path
-          if ((need & ~pmask) || t - pt0 >= pS) {
-            plo = __ffs(need) - 1;
-            pw = 32 - __clz(need) - plo;
-            // sj = lane / pw, exact: (lane + 1/2) / pw is >= 1/(2 pw) away from an integer
-            const int sj = (int)(((float)lane + 0.5f) * __frcp_rn((float)pw));
-            const uint4 u4 = philox_group_lazy(ws->key, gq, plo + lane - sj * pw, t + sj, k, ws->srho);
-            wreg = sel4(u4, bb);
-            lreg = logit_f32(wreg);
-            pt0 = t;
-            pS = (int)(32.5f * __frcp_rn((float)pw));
-            pmask = (pw == 32) ? kFull : (((1u << pw) - 1u) << plo);
-            nphil += 32u;
-          }
-          const int src = ((t - pt0) * pw + lane - plo) & 31;
-          const float l = __shfl_sync(kFull, lreg, src);
-          const float el = kLogitAbs + kLogitRel * fabsf(l);
-          bool band = false;                              // inside the fp32 error band: fp64 below
-          if (mine && !sat) {
-            const float d = z - l;
-            nx = d > 0.0f;
-            band = !(fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f);
-          }
-          if (__any_sync(kFull, band)) {                  // rare: the raw word for the fp64 path
-            const uint32_t w = __shfl_sync(kFull, wreg, src);
+          if (!need) break;                               // b quiet: general path
+          const uint32_t fs = __ballot_sync(kFull, mine && sat && (z > 0.0f) != xb);   // saturated flips at t
+          const int plo = __ffs(need) - 1;
+          const int pw = 32 - __clz(need) - plo;
+          // sj = lane / pw, exact: (lane + 1/2) / pw is >= 1/(2 pw) away from an integer
+          const int sj = (int)(((float)lane + 0.5f) * __frcp_rn((float)pw));
+          const int sp = plo + lane - sj * pw;
+          const int pS = min((int)(32.5f * __frcp_rn((float)pw)), a.T - t);
+          const bool valid = sj < pS;
+          const float z1j = __shfl_sync(kFull, z1, sp), S1j = __shfl_sync(kFull, S1, sp);
+          const int xbj = __shfl_sync(kFull, (int)xb, sp);
+          const float tfj = tf + (float)sj;               // exact
+          const float zj = tfj * z1j, Sj = tfj * S1j;
+          const bool satj = fabsf(zj) * kZScale - Sj > kSatThr20;
+          const uint32_t w = sel4(philox_group_lazy(ws->key, gq, sp, t + sj, k, ws->srho), bb);
+          const float l = logit_f32(w);
+          nphil += 32u;
+          const float d = zj - l;
+          int nxj = satj ? (zj > 0.0f) : (d > 0.0f);
+          const bool band = valid && !satj &&
+                            !(fabsf(d) > (Sj * (1.0f / kZScale) + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f);
+          if (__any_sync(kFull, band)) {                  // rare: fp64 re-evaluation
+            const float phj = __shfl_sync(kFull, phib, sp), vj = __shfl_sync(kFull, v, sp);
+            const float Aj = __shfl_sync(kFull, A, sp);
             if (band) {
-              const int rs = decide_fp64(phib, v, A, t, Hp, ws, w);
-              nx = rs & 1;
+              const int rs = decide_fp64(phj, vj, Aj, t + sj, Hp, ws, w);
+              nxj = rs & 1;
               atomicAdd(&ws->cnt[kCntFp64], 1u);
               if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
             }
           }
-          const uint32_t fm = __ballot_sync(kFull, mine && nx != (int)xb);
-          uint32_t drew = need;
-          if (fm) {
-            // A single slack flip (lane L) that keeps 2r inside the certificates' window and after
-            // which the later lanes of b flip nothing is completed here; anything else (an item
-            // flip, a second flip, the window left) leaves the whole sweep to the general path.
-            const int L = __ffs(fm) - 1;
-            const float dl = __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f;
-            const float r2n = fmaf(dl + dl, __shfl_sync(kFull, A, L), r2);
-            if (32 * b + L < n || fabsf(r2n - r2c) > a.rtol2) break;
-            const float v2 = fmaf(A, sg, r2n);
-            const float z2 = tf * fmaf(k1s, phib, -fmaf(Ak2, v2, Ak3));
-            const float S2 = tf * fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v2), fabsf(Ak3)));
-            const bool mine2 = mine && lane > L;
-            const bool sat2 = fabsf(z2) * kZScale - S2 > kSatThr20;
-            int nx2 = z2 > 0.0f;
-            const uint32_t need2 = __ballot_sync(kFull, mine2 && !sat2);
-            if (need2 & ~pmask) break;                    // (words not at hand: general path)
-            bool band2 = false;
-            if (mine2 && !sat2) {
-              const float d = z2 - l;
-              nx2 = d > 0.0f;
-              band2 = !(fabsf(d) > (S2 * (1.0f / kZScale) + el) * 1.0001f);
-            }
-            if (__any_sync(kFull, band2)) {
-              const uint32_t w = __shfl_sync(kFull, wreg, src);
-              if (band2) {
-                const int rs = decide_fp64(phib, v2, A, t, Hp, ws, w);
-                nx2 = rs & 1;
-                atomicAdd(&ws->cnt[kCntFp64], 1u);
-                if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
-              }
-            }
-            if (__ballot_sync(kFull, mine2 && nx2 != (int)xb)) break;
-            r2 = r2n;                                     // apply the slack flip: r += delta A_L
-            if (lane == L) {
-              xm ^= (1u << b);
-              if constexpr (!PK) phs[32 * b] = -phs[32 * b];
-              asg[32 * b] = -asg[32 * b];
-              xb = !xb;
-              sg = -sg;
-            }
-            v = fmaf(A, sg, r2);
-            z1 = fmaf(k1s, phib, -fmaf(Ak2, v, Ak3));
-            S1 = fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v), fabsf(Ak3)));
-            ++nflip;
-            drew |= need2;
+          const uint32_t fmj = __ballot_sync(kFull, valid && nxj != xbj);
+          const uint32_t ndj = __ballot_sync(kFull, valid && !satj);
+          // cf = first sweep of the step with a flip, q = first sweep in which every lane of b is
+          // saturated (pS if none): the step completes sweeps [t, t + min(cf, q))
+          const uint32_t grp = (pw == 32) ? kFull : ((1u << pw) - 1u);
+          const int cf = fs ? 0 : (fmj ? __shfl_sync(kFull, sj, __ffs(fmj) - 1) : pS);
+          const uint32_t qv = __ballot_sync(kFull, valid && sp == plo && ((ndj >> ((sj * pw) & 31)) & grp) == 0u);
+          const int q = qv ? __shfl_sync(kFull, sj, __ffs(qv) - 1) : pS;
+          const int c = min(cf, q);
+          const int cw = c * pw;
+          nunif += __popc(cw >= 32 ? ndj : (ndj & ((1u << cw) - 1u)));
+          t += c;
+          tf += (float)c;
+          if (c == pS) continue;                          // pS clean sweeps
+          if (q == c) break;                              // b quiet at t: the general path certifies it
+          // Sweep t has a flip; the first one in spin order is lane L.  (cw < 32 here.)
+          const uint32_t F = (((fmj >> cw) & grp) << plo) | fs;
+          const int L = __ffs(F) - 1;
+          const float dl = __shfl_sync(kFull, (int)xb, L) ? -1.0f : 1.0f;
+          const float r2n = fmaf(dl + dl, __shfl_sync(kFull, A, L), r2);
+          if (32 * b + L < n || fabsf(r2n - r2c) > a.rtol2) break;
+          // A single slack flip inside the certificates' window: the later lanes of b are
+          // re-evaluated on the new r with the same uniforms (held by lanes cw + lane - plo)
+          const float v2 = fmaf(A, sg, r2n);
+          const float z2 = tf * fmaf(k1s, phib, -fmaf(Ak2, v2, Ak3));
+          const float S2 = tf * fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v2), fabsf(Ak3)));
+          const bool mine2 = mine && lane > L;
+          const bool sat2 = fabsf(z2) * kZScale - S2 > kSatThr20;
+          int nx2 = z2 > 0.0f;
+          const uint32_t need2 = __ballot_sync(kFull, mine2 && !sat2);
+          if (need2 & ~(grp << plo)) break;               // (words not at hand: general path)
+          const int src = (cw + lane - plo) & 31;
+          const float l2 = __shfl_sync(kFull, l, src);
+          bool band2 = false;
+          if (mine2 && !sat2) {
+            const float d2 = z2 - l2;
+            nx2 = d2 > 0.0f;
+            band2 = !(fabsf(d2) > (S2 * (1.0f / kZScale) + kLogitAbs + kLogitRel * fabsf(l2)) * 1.0001f);
           }
-          nunif += __popc(drew);
+          if (__any_sync(kFull, band2)) {
+            const uint32_t w2 = __shfl_sync(kFull, w, src);
+            if (band2) {
+              const int rs = decide_fp64(phib, v2, A, t, Hp, ws, w2);
+              nx2 = rs & 1;
+              atomicAdd(&ws->cnt[kCntFp64], 1u);
+              if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
+            }
+          }
+          if (__ballot_sync(kFull, mine2 && nx2 != (int)xb)) break;
+          r2 = r2n;                                       // apply the slack flip: r += delta A_L
+          if (lane == L) {
+            xm ^= (1u << b);
+            if constexpr (!PK) phs[32 * b] = -phs[32 * b];
+            asg[32 * b] = -asg[32 * b];
+            xb = !xb;
+            sg = -sg;
+          }
+          v = fmaf(A, sg, r2);
+          z1 = fmaf(k1s, phib, -fmaf(Ak2, v, Ak3));
+          S1 = fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v), fabsf(Ak3)));
+          ++nflip;
+          nunif += __popc((((ndj >> cw) & grp) << plo) | need2);
+          ++t;
+          tf += 1.0f;
         }
         if (t >= a.T) break;
       }
