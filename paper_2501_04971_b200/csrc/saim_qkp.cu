@@ -54,6 +54,12 @@ constexpr float kSatThr20 = kSatThr * 1048576.0f;     // exact (power-of-two sca
 // 28 warps x 32 lanes: one CTA of 28 replicas per SM covers 4096 replicas in one wave (<= 72 regs).
 constexpr int kQkpMaxThreads = 896;
 
+// kDivMagic[p] = ceil(2^16 / p): (x * kDivMagic[p]) >> 16 == x / p for all x <= 32, p in [1, 32]
+// (checked exhaustively; tests/test_abi.py)
+__constant__ uint32_t kDivMagic[33] = {
+    0,     65536, 32768, 21846, 16384, 13108, 10923, 9363, 8192, 7282, 6554, 5958, 5462, 5042, 4682, 4370, 4096,
+    3856,  3641,  3450,  3277,  3121,  2979,  2850,  2731, 2622, 2521, 2428, 2341, 2260, 2185, 2115, 2048};
+
 __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
   return i == 0 ? u.x : (i == 1 ? u.y : (i == 2 ? u.z : u.w));
 }
@@ -345,17 +351,19 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           const uint32_t fs = __ballot_sync(kFull, mine && sat && (z > 0.0f) != xb);   // saturated flips at t
           const int plo = __ffs(need) - 1;
           const int pw = 32 - __clz(need) - plo;
-          // sj = lane / pw, exact: (lane + 1/2) / pw is >= 1/(2 pw) away from an integer
-          const int sj = (int)(((float)lane + 0.5f) * __frcp_rn((float)pw));
+          const uint32_t dm = kDivMagic[pw];
+          const int sj = (int)(((uint32_t)lane * dm) >> 16);   // lane / pw
           const int sp = plo + lane - sj * pw;
-          const int pS = min((int)(32.5f * __frcp_rn((float)pw)), a.T - t);
+          const int pS = min((int)((32u * dm) >> 16), a.T - t);
           const bool valid = sj < pS;
           const float z1j = __shfl_sync(kFull, z1, sp), S1j = __shfl_sync(kFull, S1, sp);
           const int xbj = __shfl_sync(kFull, (int)xb, sp);
           const float tfj = tf + (float)sj;               // exact
           const float zj = tfj * z1j, Sj = tfj * S1j;
           const bool satj = fabsf(zj) * kZScale - Sj > kSatThr20;
-          const uint32_t w = sel4(philox_group_lazy(ws->key, gq, sp, t + sj, k, ws->srho), bb);
+          // R2 counter of (spin 32 b + sp, sweep t + sj); key schedule from the parameter bank
+          const uint32_t w = sel4(philox4x32_10_ks(make_uint4(32u * (uint32_t)gq + (uint32_t)sp, (uint32_t)(t + sj),
+                                                              (uint32_t)k, ws->srho), a.ks), bb);
           const float l = logit_f32(w);
           nphil += 32u;
           const float d = zj - l;

@@ -73,3 +73,16 @@ def test_create_rejects_bad_input_without_gpu():
         with pytest.raises(P.SaimError) as ei:                              # unknown / conflicting flags
             P.Solver(None, [0, 0], [[1, 1], [1, 0]], [3, 1], 1.0, 1.0, 1.0, flags=bad)
         assert ei.value.code == P.SAIM_EINVAL
+
+
+def test_qkp_div_magic_table_is_exact():
+    """The QKP hot step divides lane indices by the unsaturated width pw with the table
+    kDivMagic[p] = ceil(2^16 / p) (saim_qkp.cu): (x * m) >> 16 == x // p for every x <= 32."""
+    import re
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2501_04971_b200", "csrc", "saim_qkp.cu")).read()
+    body = re.search(r"kDivMagic\[33\]\s*=\s*\{([^}]*)\}", src).group(1)
+    mag = [int(v) for v in body.replace("\n", " ").split(",") if v.strip()]
+    assert len(mag) == 33
+    for p in range(1, 33):
+        for x in range(33):
+            assert (x * mag[p]) >> 16 == x // p, (p, x)
