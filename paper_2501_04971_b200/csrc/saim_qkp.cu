@@ -104,12 +104,14 @@ __device__ __noinline__ int decide_fp64(float phib, float v, float A, int t, con
   return (d > 0.0 ? 1 : 0) | (fabs(d) <= e ? 2 : 0);
 }
 
-// Lazily drawn uniforms: the empty volatile asm is a side effect, so the compiler cannot
-// speculatively hoist the 10-round Philox into the common (saturated) path.
-__device__ __forceinline__ uint4 philox_group_lazy(uint2 key, int g, int lane, int t, int k, uint32_t srho) {
+// Lazily drawn uniforms of a group (key schedule from the kernel-parameter bank, RunArgs::ks):
+// the empty volatile asm is a side effect, so the compiler cannot speculatively hoist the
+// 10-round Philox into the common (saturated) path.
+__device__ __forceinline__ uint4 philox_group_lazy_ks(const uint32_t (&ks)[20], int g, int lane, int t, int k,
+                                                      uint32_t srho) {
   uint32_t x = 32u * (uint32_t)g + (uint32_t)lane;
   asm volatile("" : "+r"(x));
-  return philox4x32_10(make_uint4(x, (uint32_t)t, (uint32_t)k, srho), key);
+  return philox4x32_10_ks(make_uint4(x, (uint32_t)t, (uint32_t)k, srho), ks);
 }
 
 }  // namespace
@@ -250,20 +252,19 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
                 phw[32 * (2 * w + h)] = phw[32 * (2 * w + h)] + __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) - 0x00800080u;
           }
         }
-        ++nflip;
-        return;
-      }
+      } else {
 #pragma unroll
-      for (int w = 0; w < QW; ++w) {
-        const uint32_t word = row[32 * w];
+        for (int w = 0; w < QW; ++w) {
+          const uint32_t word = row[32 * w];
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int m = E * w + e;
-          if (m < NPL) {
-            const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
-            const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
-            const float sdl = ((xm >> m) & 1u) ? dl : -dl;           // (2x_i - 1) delta
-            phs[32 * m] = fmaf(-sdl, q, phs[32 * m]);
+          for (int e = 0; e < E; ++e) {
+            const int m = E * w + e;
+            if (m < NPL) {
+              const uint32_t selr = (QB == 1) ? (0x7650u | (uint32_t)e) : (0x7600u | ((2u * e + 1u) << 4) | (2u * e));
+              const float q = __uint_as_float(__byte_perm(word, 0x4B000000u, selr)) - (8388608.0f + kQBias);
+              const float sdl = ((xm >> m) & 1u) ? dl : -dl;           // (2x_i - 1) delta
+              phs[32 * m] = fmaf(-sdl, q, phs[32 * m]);
+            }
           }
         }
       }
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         if (gb & ~m) certify((gb & ~m) << (4 * g));        // scanned and quiet: certified
         if (m) {
           // the group's uniform words, drawn once per visit of a group with a non-quiet block
-          const uint4 u4 = philox_group_lazy(ws->key, g, lane, t, k, ws->srho);
+          const uint4 u4 = philox_group_lazy_ks(a.ks, g, lane, t, k, ws->srho);
           ws->uw[0][lane] = u4.x; ws->uw[1][lane] = u4.y; ws->uw[2][lane] = u4.z; ws->uw[3][lane] = u4.w;
           __syncwarp();
           nphil += 32u;
