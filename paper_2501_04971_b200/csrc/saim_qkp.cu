@@ -284,23 +284,88 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (a.T >= 2) {
       // ---- sweep t = 0: beta_0 = 0, x_i = [u < 1/2] (state-independent; R3, R5) ----
       t0 = 1;
-      for (int g = 0; g < NG; ++g) {
-        const uint4 uw = philox_group(ws->key, g, lane, 0, k, ws->srho);
-        cnt_add(ws, kCntPhilox, 32);
+      if constexpr (PK) {
+        // Every decision of sweep 0 is state-independent, so the new state x' is known at once
+        // and phi' = phi - sum over flipped items j of delta_j Q_j: the Q rows are summed into
+        // packed registers (exact integer sums in any order; every partial sum is phi of the state
+        // with the flips added so far, so it stays within the proven |phi| bound and no 16-bit
+        // half carries).
+        uint32_t xn = 0;                                  // bit b = x'_{32b + lane}
+        for (int g = 0; g < NG; ++g) {
+          const uint4 uw = philox_group_lazy_ks(a.ks, g, lane, 0, k, ws->srho);
+          cnt_add(ws, kCntPhilox, 32);
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb) {
-          const int b = 4 * g + bb;
-          if (b < NB) {
-            const bool valid = lane < N - 32 * b;
-            const int xb = (xm >> b) & 1u;
-            const int nx = (sel4(uw, bb) >> 31) == 0u;   // u < 1/2  <=>  w < 2^31
-            uint32_t fm = __ballot_sync(kFull, valid && nx != xb);
-            cnt_add(ws, kCntUnif, __popc(__ballot_sync(kFull, valid)));
-            const float A = sAl[32 * b];
-            while (fm) {
-              const int L = __ffs(fm) - 1;
-              fm &= fm - 1u;
-              apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+          for (int bb = 0; bb < 4; ++bb) {
+            const int b = 4 * g + bb;
+            if (b < NB) {
+              const bool valid = lane < N - 32 * b;
+              if (valid && (sel4(uw, bb) >> 31) == 0u) xn |= 1u << b;   // u < 1/2  <=>  w < 2^31
+              cnt_add(ws, kCntUnif, __popc(__ballot_sync(kFull, valid)));
+            }
+          }
+        }
+        const uint32_t dx = xn ^ xm;                      // flipped blocks of this lane
+        constexpr int PW = (NPL + 1) / 2;                 // packed phi words holding items
+        uint32_t acc[PW];
+#pragma unroll
+        for (int p = 0; p < PW; ++p) acc[p] = phw[32 * p];
+        for (int b = 0; b < NPL; ++b) {
+          uint32_t fb = __ballot_sync(kFull, ((dx >> b) & 1u) && 32 * b + lane < n);
+          const uint32_t up = __ballot_sync(kFull, (xn >> b) & 1u);
+          while (fb) {
+            const int L = __ffs(fb) - 1;
+            fb &= fb - 1u;
+            const uint32_t *row = sQl + (32 * b + L) * (QW * 32);
+            if ((up >> L) & 1u) {                         // 0 -> 1: phi -= Q_j
+#pragma unroll
+              for (int w = 0; w < QW; ++w) {
+                const uint32_t word = row[32 * w];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  if (2 * w + h < PW) acc[2 * w + h] = acc[2 * w + h] - __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) + 0x00800080u;
+              }
+            } else {                                      // 1 -> 0: phi += Q_j
+#pragma unroll
+              for (int w = 0; w < QW; ++w) {
+                const uint32_t word = row[32 * w];
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  if (2 * w + h < PW) acc[2 * w + h] = acc[2 * w + h] + __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) - 0x00800080u;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < PW; ++p) phw[32 * p] = acc[p];
+        int load = 0;                                     // sum_i A_ext,i x'_i (exact)
+#pragma unroll
+        for (int m = 0; m < NBP; ++m) {
+          if ((dx >> m) & 1u) asg[32 * m] = -asg[32 * m];
+          if ((xn >> m) & 1u) load += (int)sAl[32 * m];
+          nflip += __popc(__ballot_sync(kFull, (dx >> m) & 1u));
+        }
+        load = __reduce_add_sync(kFull, load);
+        xm = xn;
+        if (has_con) r2 = (float)(2 * ((long long)load - Hp->b0));
+      } else {
+        for (int g = 0; g < NG; ++g) {
+          const uint4 uw = philox_group(ws->key, g, lane, 0, k, ws->srho);
+          cnt_add(ws, kCntPhilox, 32);
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int b = 4 * g + bb;
+            if (b < NB) {
+              const bool valid = lane < N - 32 * b;
+              const int xb = (xm >> b) & 1u;
+              const int nx = (sel4(uw, bb) >> 31) == 0u;   // u < 1/2  <=>  w < 2^31
+              uint32_t fm = __ballot_sync(kFull, valid && nx != xb);
+              cnt_add(ws, kCntUnif, __popc(__ballot_sync(kFull, valid)));
+              const float A = sAl[32 * b];
+              while (fm) {
+                const int L = __ffs(fm) - 1;
+                fm &= fm - 1u;
+                apply_flip(b, L, __shfl_sync(kFull, A, L), __shfl_sync(kFull, nx, L) ? 1.0f : -1.0f);
+              }
             }
           }
         }
