@@ -251,18 +251,20 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // with the band value G_i = A_i . A_{i-1}:  A_i . r_now = pre + delta_{i-1} G_i.
       auto dots = [&](int i, float &pr, float &dlv) {
         const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
-        float dr0 = 0.f, dr1 = 0.f, dl0 = 0.f, dl1 = 0.f;
+        // four partial sums per dot product (short dependency chains; each term still passes at
+        // most MA/4 + 2 roundings, inside the (MM + 8) 2^-24 bound of E1)
+        float dr0 = 0.f, dr1 = 0.f, dr2 = 0.f, dr3 = 0.f, dl0 = 0.f, dl1 = 0.f, dl2 = 0.f, dl3 = 0.f;
 #pragma unroll
         for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
           const float4 av = Ac[m4];
           dr0 = fmaf(av.x, r[4 * m4 + 0], dr0);
           dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0);
           if (4 * m4 + 1 < MA) { dr1 = fmaf(av.y, r[4 * m4 + 1], dr1); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1); }
-          if (4 * m4 + 2 < MA) { dr0 = fmaf(av.z, r[4 * m4 + 2], dr0); dl0 = fmaf(av.z, cL[4 * m4 + 2], dl0); }
-          if (4 * m4 + 3 < MA) { dr1 = fmaf(av.w, r[4 * m4 + 3], dr1); dl1 = fmaf(av.w, cL[4 * m4 + 3], dl1); }
+          if (4 * m4 + 2 < MA) { dr2 = fmaf(av.z, r[4 * m4 + 2], dr2); dl2 = fmaf(av.z, cL[4 * m4 + 2], dl2); }
+          if (4 * m4 + 3 < MA) { dr3 = fmaf(av.w, r[4 * m4 + 3], dr3); dl3 = fmaf(av.w, cL[4 * m4 + 3], dl3); }
         }
-        pr = dr0 + dr1;
-        dlv = dl0 + dl1;
+        pr = (dr0 + dr1) + (dr2 + dr3);
+        dlv = (dl0 + dl1) + (dl2 + dl3);
       };
       float pre = 0.f, dlc = 0.f, dprev = 0.f, Gc = 0.f;
       dots(0, pre, dlc);                                  // (column n is zero: the lookahead past n-1 is harmless)
