@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   uint32_t xm = 0;                                  // bit b = x_{32b + lane}
   uint32_t nflip = 0;                               // flips so far (warp-uniform)
   uint32_t qmask = 0;                               // blocks certified quiet since the last flip
+  uint32_t dense = 0;                               // groups processed without scans (bit g)
   uint32_t nunif = 0, nphil = 0;                    // uniforms drawn, lazy Philox calls x 32 (sweeps t >= 1)
   float r2 = has_con ? (float)(-2 * Hp->b0) : 0.0f; // 2r, r = A_ext x - b (exact integer)
 
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     const bool freeze_exit = !(a.flags & SAIM_FLAG_NO_FREEZE_EXIT);
     const bool hot_loop = a.T >= 2 && !(a.flags & SAIM_FLAG_QKP_NO_HOT_LOOP);
     qmask = 0u;                                         // new Lambda_k: every group is scanned again
+    dense = 0u;
     for (int t = t0; t < a.T; ++t) {
 #ifdef SAIM_PROF
       const long long prof_c0 = clock64();
@@ -524,8 +526,8 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
 
       // Exact sequential processing of block b (bb = b % 4) from the current state: rounds of
       // evaluate -> ballot first flipper -> flip, until every lane of the block is decided.
-      // Returns true if a spin of the block flipped.
-      auto process_block = [&](int b, int bb) -> bool {
+      // Returns bit 0: a spin of the block flipped; bit 1: some lane was not saturated.
+      auto process_block = [&](int b, int bb) -> int {
         const int hi = N - 32 * b;                        // lanes < hi hold a spin
         const float A = sAl[32 * b];
         const bool xb = (xm >> b) & 1u;
@@ -575,7 +577,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           if (lo >= hi) break;
         }
         nunif += __popc(drew);
-        return flipped;
+        return (flipped ? 1 : 0) | (drew ? 2 : 0);
       };
 
       // Speculative scan of one block on the current state: bit bb of nq is set if this lane's
@@ -594,14 +596,24 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       };
       // Process the non-quiet blocks of group g in order (exactly); after a flip the later
       // blocks' speculation is stale, so they are rescanned.
-      auto handle_group = [&](uint32_t m) {
+      // Dense groups (DESIGN.md 6.1 "Dense groups", dg): while every block of group g is
+      // non-quiet (early in an anneal), its blocks are processed in order with no rescan after a
+      // flip -- process_block alone decides every spin exactly; the first block found entirely
+      // saturated with no flip sends the group back to scanning.
+      auto handle_group = [&](uint32_t m, bool dg) {
         active = true;
         for (;;) {
           int bstart = 4;
           while (m) {
             const int bb = __ffs(m) - 1;
             m &= m - 1u;
-            if (process_block(4 * g + bb, bb)) { bstart = bb + 1; break; }
+            const int st = process_block(4 * g + bb, bb);
+            if (dg) {
+              if (!st) dense &= ~(1u << g);
+            } else if (st & 1) {
+              bstart = bb + 1;
+              break;
+            }
           }
           if (bstart >= 4) return;
           uint32_t nq = 0;
@@ -623,15 +635,17 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         g = (__ffs(todo) - 1) >> 2;
         const uint32_t gb = (todo >> (4 * g)) & 15u;        // blocks of group g to scan
         todo &= ~(15u << (4 * g));
-        uint32_t nq = 0;
+        const bool dg = (dense >> g) & 1u;
+        uint32_t m = gb;
+        if (!dg) {
+          uint32_t nq = 0;
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
-          if ((gb >> bb) & 1u) scan_one(nq, 4 * g + bb, bb);
-        const uint32_t m = __reduce_or_sync(kFull, nq);
-#ifdef SAIM_STATS
-        cnt_add(ws, kCntUncert, 1);
-#endif
-        if (gb & ~m) certify((gb & ~m) << (4 * g));        // scanned and quiet: certified
+          for (int bb = 0; bb < 4; ++bb)
+            if ((gb >> bb) & 1u) scan_one(nq, 4 * g + bb, bb);
+          m = __reduce_or_sync(kFull, nq);
+          if (gb & ~m) certify((gb & ~m) << (4 * g));      // scanned and quiet: certified
+          if (m == gb && gb == ((allb >> (4 * g)) & 15u)) dense |= 1u << g;   // no quiet block: dense
+        }
         if (m) {
           // the group's uniform words, drawn once per visit of a group with a non-quiet block
           const uint4 u4 = philox_group_lazy_ks(a.ks, g, lane, t, k, ws->srho);
@@ -639,7 +653,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           __syncwarp();
           nphil += 32u;
           const uint32_t nf0 = nflip;
-          handle_group(m);
+          handle_group(m, dg);
           if (nflip != nf0) {
             // item flips voided the certificates; slack flips only moved r -- the certificates
             // hold while 2r stays within the tolerance (checked before a certified block is skipped)
