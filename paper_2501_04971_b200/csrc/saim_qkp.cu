@@ -534,9 +534,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         const float AK2 = A * K2, AK3 = A * K3;
         const float sg = xb ? -1.0f : 1.0f;              // 1 - 2x_i
         bool flipped = false;
-        bool have_l = false;                              // logit of this lane's u, drawn once per visit
-        float l = 0.0f, el = 0.0f;
-        uint32_t w = 0;
+        // logit of this lane's uniform, once per visit (99.8% of visits need some lane's at config 2)
+        const uint32_t w = ws->uw[bb][lane];
+        const float l = logit_f32(w);
+        const float el = kLogitAbs + kLogitRel * fabsf(l);
         uint32_t drew = 0;                                // lanes that needed their uniform in this visit
         int lo = 0;                                       // lanes in [lo, hi) are still pending
         for (;;) {
@@ -549,12 +550,6 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           int nx = z > 0.0f;
           const uint32_t need = __ballot_sync(kFull, mine && !sat);
           if (need) {
-            if (!have_l) {
-              w = ws->uw[bb][lane];
-              l = logit_f32(w);
-              el = kLogitAbs + kLogitRel * fabsf(l);
-              have_l = true;
-            }
             drew |= need;
             if (mine && !sat) {
               const float d = z - l;
