@@ -404,6 +404,11 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         float z1 = fmaf(k1s, phib, -fmaf(Ak2, v, Ak3));
         float S1 = fmaf(k1s, fabsf(phib), fmaf(fabsf(Ak2), fabsf(v), fabsf(Ak3)));
         float tf = (float)t;                                // exact (t < 2^24)
+        // the current window: sweeps [wb, wb + pS), lane j holding spin lane sp = plo + j % pw at
+        // sweep wb + sj (sj = j / pw), its Philox word w and logit l
+        int wb = -1, plo = 0, pw = 32, sj = 0, sp = 0, pS = 0;
+        uint32_t grp = kFull, w = 0;
+        float l = 0.0f;
         for (; t < a.T;) {
           // One step covers sweeps [t, t + pS): on sweep t the saturated lanes of b are certified
           // for every later sweep too (constant fields, |z| = t |z1| grows with t); the pw lanes
@@ -417,23 +422,31 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           const uint32_t need = __ballot_sync(kFull, mine && !sat);
           if (!need) break;                               // b quiet: general path
           const uint32_t fs = __ballot_sync(kFull, mine && sat && (z > 0.0f) != xb);   // saturated flips at t
-          const int plo = __ffs(need) - 1;
-          const int pw = 32 - __clz(need) - plo;
-          const uint32_t dm = kDivMagic[pw];
-          const int sj = (int)(((uint32_t)lane * dm) >> 16);   // lane / pw
-          const int sp = plo + lane - sj * pw;
-          const int pS = min((int)((32u * dm) >> 16), a.T - t);
-          const bool valid = sj < pS;
+          // A new window unless the current one still covers sweep t and every unsaturated lane
+          // (after an in-place slack flip the later sweeps' words stay valid: uniforms depend on
+          // (spin, sweep) only)
+          if (wb < 0 || t - wb >= pS || (need & ~(grp << plo))) {
+            plo = __ffs(need) - 1;
+            pw = 32 - __clz(need) - plo;
+            const uint32_t dm = kDivMagic[pw];
+            sj = (int)(((uint32_t)lane * dm) >> 16);      // lane / pw
+            sp = plo + lane - sj * pw;
+            pS = min((int)((32u * dm) >> 16), a.T - t);
+            grp = (pw == 32) ? kFull : ((1u << pw) - 1u);
+            wb = t;
+            // R2 counter of (spin 32 b + sp, sweep t + sj); key schedule from the parameter bank
+            w = sel4(philox4x32_10_ks(make_uint4(32u * (uint32_t)gq + (uint32_t)sp, (uint32_t)(t + sj), (uint32_t)k,
+                                                 ws->srho), a.ks), bb);
+            l = logit_f32(w);
+            nphil += 32u;
+          }
+          const int c0 = t - wb;                          // first sweep of the window still open
+          const bool valid = sj >= c0 && sj < pS;
           const float z1j = __shfl_sync(kFull, z1, sp), S1j = __shfl_sync(kFull, S1, sp);
           const int xbj = __shfl_sync(kFull, (int)xb, sp);
-          const float tfj = tf + (float)sj;               // exact
+          const float tfj = (float)(wb + sj);             // exact
           const float zj = tfj * z1j, Sj = tfj * S1j;
           const bool satj = fabsf(zj) * kZScale - Sj > kSatThr20;
-          // R2 counter of (spin 32 b + sp, sweep t + sj); key schedule from the parameter bank
-          const uint32_t w = sel4(philox4x32_10_ks(make_uint4(32u * (uint32_t)gq + (uint32_t)sp, (uint32_t)(t + sj),
-                                                              (uint32_t)k, ws->srho), a.ks), bb);
-          const float l = logit_f32(w);
-          nphil += 32u;
           const float d = zj - l;
           int nxj = satj ? (zj > 0.0f) : (d > 0.0f);
           const bool band = valid && !satj &&
@@ -442,7 +455,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             const float phj = __shfl_sync(kFull, phib, sp), vj = __shfl_sync(kFull, v, sp);
             const float Aj = __shfl_sync(kFull, A, sp);
             if (band) {
-              const int rs = decide_fp64(phj, vj, Aj, t + sj, Hp, ws, w);
+              const int rs = decide_fp64(phj, vj, Aj, wb + sj, Hp, ws, w);
               nxj = rs & 1;
               atomicAdd(&ws->cnt[kCntFp64], 1u);
               if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
@@ -450,18 +463,17 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           }
           const uint32_t fmj = __ballot_sync(kFull, valid && nxj != xbj);
           const uint32_t ndj = __ballot_sync(kFull, valid && !satj);
-          // cf = first sweep of the step with a flip, q = first sweep in which every lane of b is
-          // saturated (pS if none): the step completes sweeps [t, t + min(cf, q))
-          const uint32_t grp = (pw == 32) ? kFull : ((1u << pw) - 1u);
-          const int cf = fs ? 0 : (fmj ? __shfl_sync(kFull, sj, __ffs(fmj) - 1) : pS);
+          // cf = first window sweep (>= c0) with a flip, q = first one in which every lane of b is
+          // saturated (pS if none): sweeps [wb + c0, wb + min(cf, q)) are complete
+          const int cf = fs ? c0 : (fmj ? __shfl_sync(kFull, sj, __ffs(fmj) - 1) : pS);
           const uint32_t qv = __ballot_sync(kFull, valid && sp == plo && ((ndj >> ((sj * pw) & 31)) & grp) == 0u);
           const int q = qv ? __shfl_sync(kFull, sj, __ffs(qv) - 1) : pS;
           const int c = min(cf, q);
           const int cw = c * pw;
-          nunif += __popc(cw >= 32 ? ndj : (ndj & ((1u << cw) - 1u)));
-          t += c;
-          tf += (float)c;
-          if (c == pS) continue;                          // pS clean sweeps
+          nunif += __popc(cw >= 32 ? ndj : (ndj & ((1u << cw) - 1u)));   // (bits below c0 pw are 0)
+          t = wb + c;
+          tf = (float)t;
+          if (c == pS) { wb = -1; continue; }             // window done
           if (q == c) break;                              // b quiet at t: the general path certifies it
           // Sweep t has a flip; the first one in spin order is lane L.  (cw < 32 here.)
           const uint32_t F = (((fmj >> cw) & grp) << plo) | fs;
