@@ -178,6 +178,21 @@ def test_parity_edge_cases(P):
     run_both(P, [p], [0.01], 0.001, 0.05, seed=9, R=8, K=4, T=50)
 
 
+@pytest.mark.parametrize("c0,packed", [(-32667, 1), (-32668, 0)])
+def test_packed_phi_boundary(P, c0, packed):
+    """phi is held as biased int16 pairs iff max_i |c_i| + sum_j |Q_ij| <= 32767 (saim_api.cu);
+    at the boundary phi reaches +-32767 (biased 1 / 65535), still bit-exact against the oracle."""
+    p = _qkp(40, 0.5, 21)
+    p.Q[0, :] = 0
+    p.Q[:, 0] = 0
+    p.Q[0, 1] = p.Q[1, 0] = -100
+    p.c[0] = c0
+    p.Q[1, 2:] = 0
+    p.Q[2:, 1] = 0
+    g = run_both(P, [p], [si.paper_P(p, 2.0)], 20.0, 10.0, seed=22, R=8, K=3, T=30)
+    assert g["info"]["phi_packed"] == packed
+
+
 def test_parity_multi_instance_batch(P):
     """Instances with different N (different slack counts) in one launch; RNG keyed on instance."""
     probs = [_qkp(60, 0.5, s, cap=c) for s, c in enumerate([3, 200, 1500, 70000 // 50])]
