@@ -1,7 +1,7 @@
 """One-off parity evidence at a BASELINE config's full size: the GPU run of all replicas against the
 threaded oracle on a contiguous block of replicas (every per-iteration readout x_k, f, feasibility,
 r, Lambda, the best sample, the final state and the block's total flip count).
-python tools/parity_sample.py --config 2 --seed 7 --start 0 --count 512"""
+python tests/parity_sample.py --config 2 --seed 7 --start 0 --count 512"""
 import argparse
 import json
 import os
@@ -10,7 +10,7 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 
 def main():

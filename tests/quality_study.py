@@ -5,7 +5,7 @@ Table II), reporting the paper's metrics: feasibility %, best
 accuracy of feasible samples.  OPT is exact (brute force) for n <= 24; otherwise accuracy is
 relative to the best feasible cost found by any run (labelled "best-known").
 
-  python tools/quality.py [--R 64] [--K 2000] [--T 1000]
+  python tests/quality_study.py [--R 64] [--K 2000] [--T 1000]
 """
 import argparse
 import json
