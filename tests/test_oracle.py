@@ -391,3 +391,74 @@ def test_penalty_baseline_is_eta_zero():
     a = oracle.OracleProblem.from_inputs(prob, cfg.P[0], 0.0, cfg.beta_max).run(seed=3, nrep=4, K=1, T=50, trace=True)
     b = oracle.OracleProblem.from_inputs(prob, cfg.P[0], 20.0, cfg.beta_max).run(seed=3, nrep=4, K=1, T=50, trace=True)
     assert np.array_equal(a["tr_x"], b["tr_x"])
+
+
+# ---------------------------------------------------------------------------------------------
+# The linear beta ramp ("a linear beta-schedule swept from 0 to beta_max";
+# DESIGN.md R3: beta_t = beta_max t/(T-1), so beta_{T-1} = beta_max and beta at t = (T-1)/2 is
+# beta_max/2).  The pins use the exact predicate u < sigma(beta_t F) with beta_t an exact rational.
+
+def _odd_u_near(sig: float, above: bool) -> float:
+    """The representable uniform (odd numerator over 2^24, R2) just below / above sig."""
+    m = int(sig * 2 ** 24)
+    if m % 2 == 0:
+        m += -1 if not above else 1
+    elif above:
+        m += 2
+    u = m / 2.0 ** 24
+    assert (u > sig) == above
+    return u
+
+
+@pytest.mark.parametrize("T", [2, 5, 101, 1000])
+def test_beta_ramp_endpoints_and_interior(T):
+    """fp64 path: for u one representable step below / above sigma(beta_t F), the decision is 1 / 0
+    only if beta_t = beta_max t/(T-1) to ~1e-6 relative -- a ramp t/T, or one sweep early/late,
+    flips one of the two.  Covers t = T-1 (beta_max), t = (T-1)/2 (beta_max/2) and other interior t."""
+    beta_max = 4.0
+    op = oracle.OracleProblem(None, [1], [[1]], [1], 0.0, 0.0, beta_max)   # s_o = s_c = 1, F = phi
+    ts = sorted({T - 1, (T - 1) // 2, max(1, (T - 1) // 3), 1} - {0})
+    for t in ts:
+        beta = Fraction(beta_max) * t / (T - 1)
+        if t == T - 1:
+            assert beta == beta_max
+        if 2 * t == T - 1:
+            assert beta == Fraction(beta_max) / 2
+        for phi in (1, 2, -1):
+            sig = float(sigma_exact(beta * phi))
+            for above in (False, True):
+                u = _odd_u_near(sig, above)
+                exact = int(Fraction(u) < Fraction(str(sigma_exact(beta * phi))))
+                assert exact == int(not above)
+                assert op.decide(u, t, T, phi, 0, 0) == exact, (T, t, phi, above)
+                # the neighbouring sweeps' beta (and the t/T ramp) decide differently at this u
+                for wrong in (Fraction(beta_max) * (t - 1) / (T - 1), Fraction(beta_max) * t / T):
+                    w = int(Fraction(u) < Fraction(str(sigma_exact(wrong * phi))))
+                    if phi > 0 and not above:
+                        assert w != exact
+
+
+@pytest.mark.parametrize("T", [3, 1001])
+def test_beta_ramp_binary128_path(T):
+    """Near ties at an interior and the last sweep: z = -beta_t P lands within a few fp64 ulps of
+    logit(u), so the fp64 bound cannot decide and the binary128 re-evaluation must use the same
+    beta_t = beta_max t/(T-1).  The exact answers differ across the +-ulp variants, so a wrong beta
+    (which moves z far from logit(u) and gives one answer for all of them) fails."""
+    rng = np.random.default_rng(2024 + T)
+    beta_max = 10.0
+    for t in (T - 1, (T - 1) // 2):
+        beta = Fraction(beta_max) * t / (T - 1)
+        answers = set()
+        for _ in range(40):
+            u = (2 * int(rng.integers(2 ** 20, 2 ** 23 - 2 ** 20)) + 1) / 2.0 ** 24
+            P0 = -math.log(u / (1 - u)) / float(beta)
+            for ulps in (-3, -1, 0, 1, 3):
+                Pv = P0
+                for _k in range(abs(ulps)):
+                    Pv = float(np.nextafter(Pv, math.inf if ulps > 0 else -math.inf))
+                op = oracle.OracleProblem(None, [1], [[1]], [1], Pv, 0.0, beta_max)
+                # F = -P pi with pi = 1, phi = kappa = 0: z = -beta_t P
+                exact = int(Fraction(u) < Fraction(str(sigma_exact(-beta * Fraction(Pv)))))
+                assert op.decide(u, t, T, 0, 1, 0) == exact, (T, t, u, ulps)
+                answers.add(exact)
+        assert answers == {0, 1}
