@@ -32,32 +32,54 @@ sys.path.insert(0, ROOT)
 
 import saim_inputs as si  # noqa: E402
 
-# Algorithmic lane-ops per attempted update: fast path per decision,
-# per drawn uniform (Philox4x32-10 / 4 + u map + logit + compare), per flip (n-element phi update:
-# byte extract + convert + fma, plus the Q-row loads) -- counted from the kernel's counters.
-OPS_DECISION = 8
-OPS_UNIFORM = 30
-OPS_FLIP_PER_ITEM = 3.25
-LANES_PER_SM_CLK = 128          # 4 SMSPs x 32 FP32/INT32 lanes issue per clock (B200_PROFILING.md)
+# Per-SM, per-clock peaks of the B200 pipes (tools/ubench.cu, profiles/r01/ubench_b200.txt;
+# B200_PROFILING.md unit counts): INT32 lanes, FP32 lanes, MUFU lanes, warp-instruction issue in
+# lane-ops (4 SMSPs x 32), shared-memory bytes.
+PEAK_PER_SM_CLK = {"int": 64, "fp32": 128, "mufu": 16, "issue": 128, "smem": 128}
+
+
+def roofline_model(kind, M, N, c, sm_count, clk_mhz):
+    """SURVEY.md 8(d) algorithmic op model per attempted p-bit update, path-weighted by this run's
+    counters: f_u = uniforms / decisions (unsaturated decisions), p_f = flips / decisions.
+      QKP (M <= 1): INT 4 + 18 f_u + p_f (0.75 N + M); FP32 5 + 3 f_u; MUFU f_u; SMEM p_f N bytes
+      MKP:          INT 2M + 18 f_u + p_f M;          FP32 5 + 3 f_u; MUFU f_u; SMEM 2M + 2M p_f
+    (issue = INT + FP32 + MUFU lane-ops).  The roof of each class is 148 SMs x its per-clock peak x
+    the measured SM clock / its ops per update; the smallest roof binds."""
+    dec = float(c["decisions"])
+    f_u, p_f = c["uniforms"] / dec, c["flips"] / dec
+    if kind == "qkp":
+        ops = {"int": 4 + 18 * f_u + p_f * (0.75 * N + M), "fp32": 5 + 3 * f_u, "mufu": f_u,
+               "smem": p_f * N}
+    else:
+        ops = {"int": 2 * M + 18 * f_u + p_f * M, "fp32": 5 + 3 * f_u, "mufu": f_u,
+               "smem": 2 * M + 2 * M * p_f}
+    ops["issue"] = ops["int"] + ops["fp32"] + ops["mufu"]
+    hz = clk_mhz * 1e6
+    roofs = {k: sm_count * PEAK_PER_SM_CLK[k] * hz / v for k, v in ops.items() if v > 0}
+    bind = min(roofs, key=roofs.get)
+    return {"f_u": f_u, "p_f": p_f, "ops_per_update": ops, "roof_updates_per_s": roofs, "binding": bind,
+            "peak_per_s": sm_count * PEAK_PER_SM_CLK[bind] * hz}
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def ncu_traffic_bytes():
+def ncu_traffic_bytes(config):
     """dram__bytes_read.sum + dram__bytes_write.sum of the SAIM kernel per launch, from the committed
-    ncu --set full capture of the same workload (profiles/r01/qkp_config2_K200_raw_selected.csv)."""
-    p = os.path.join(ROOT, "profiles", "r01", "qkp_config2_K200_raw_selected.csv")
-    if not os.path.exists(p):
-        return None
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tot = 0.0
-    for ln in open(p).read().splitlines()[1:]:
-        name, unit, val = ln.split(",", 2)
-        if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            tot += float(val) * scale.get(unit, 1)
-    return tot
+    ncu --set full capture of the same workload (a static artefact, not measured by this run: the
+    path is on-chip and ncu cannot run inside the timed process)."""
+    for p in (os.path.join(ROOT, "profiles", "r02", f"config{config}_ncu_raw_selected.csv"),
+              os.path.join(ROOT, "profiles", "r01", "qkp_config2_K200_raw_selected.csv") if config == 2 else ""):
+        if p and os.path.exists(p):
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            tot = 0.0
+            for ln in open(p).read().splitlines()[1:]:
+                name, unit, val = ln.split(",", 2)
+                if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    tot += float(val) * scale.get(unit, 1)
+            return tot, os.path.relpath(p, ROOT)
+    return None, None
 
 
 def measured_peaks():
@@ -130,8 +152,9 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_sample(cfg, seconds_target=15.0, threads=None, seed=1):
-    """Time the oracle (as it stands) on a bounded sample of the workload on the host's cores."""
+def oracle_sample(cfg, seconds_target=15.0, threads=None, seed=1, trace=False):
+    """Time the oracle (as it stands) on a bounded sample of the workload on the host's cores:
+    replicas [0, nrep) of instance 0, the first K = 2 Lagrange iterations."""
     import oracle
     threads = threads or os.cpu_count() or 1
     prob = cfg.instances[0]
@@ -141,16 +164,21 @@ def oracle_sample(cfg, seconds_target=15.0, threads=None, seed=1):
     t0 = time.perf_counter()
     op.run(seed, 1, 1, cfg.T, nthreads=1)
     per_rep_iter = max(time.perf_counter() - t0, 1e-3)
-    K = 2
+    K = min(2, cfg.K)
     nrep = max(threads, int(round(seconds_target * threads / (per_rep_iter * K) / threads)) * threads)
     nrep = min(nrep, cfg.R)
     t0 = time.perf_counter()
-    op.run(seed, nrep, K, cfg.T, nthreads=threads)
+    res = op.run(seed, nrep, K, cfg.T, nthreads=threads, trace=trace, final=trace)
     dt = time.perf_counter() - t0
     updates = nrep * K * cfg.T * N
     return {"updates_per_s": updates / dt, "samples_per_s": nrep * K / dt, "seconds": dt, "cores": threads,
-            "sample": f"{nrep} replicas x K={K} iterations x T={cfg.T} sweeps x N={N} spins of {cfg.name} "
-                      f"(first {K} of {cfg.K} Lagrange iterations), {threads} threads, {cpu_model()}"}
+            "nrep": nrep, "K": K, "seed": seed, "N": N, "result": res,
+            "sample": f"{nrep} replicas x K={K} iterations x T={cfg.T} sweeps x N={N} spins of instance 0 of "
+                      f"{cfg.name} (first {K} of {cfg.K} Lagrange iterations), {threads} threads, {cpu_model()}"}
+
+
+def metric_name(cfg):
+    return f"p-bit updates/sec (SAIM, {cfg.name}, BASELINE config {cfg.idx})"
 
 
 def run_reference(args):
@@ -170,12 +198,12 @@ def run_reference(args):
     v = float(np.mean(vals))
     N = si.n_spins(cfg.instances[0])
     line = {
-        "impl": "reference", "metric": "p-bit updates/sec (SAIM, QKP n=300 config 2)", "value": v,
+        "impl": "reference", "metric": metric_name(cfg), "value": v,
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * cfg.R * cfg.K * cfg.T * N / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.R} replicas x K={cfg.K} x T={cfg.T} x N={N} "
-                               "(reference arm times a bounded sample of it)"},
+        "config": {"workload": f"{cfg.name} (BASELINE config {cfg.idx}): {cfg.R} replicas x K={cfg.K} x "
+                               f"T={cfg.T} x N={N} (reference arm times a bounded sample of it)"},
         "samples_per_s": v / (cfg.T * N),
         "cpu_baseline": {"value": v, "unit": "updates/s", "cores": info["cores"], "kind": "oracle",
                          "sample": info["sample"]},
@@ -217,9 +245,12 @@ def main():
     cfg = si.config_instances(args.config)
     Q, c, A, b = si.stack(cfg.instances)
     rep0, R = sdist.shard_range(rank, world, cfg.R)   # weak scaling: own global replica range
-    sol = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    sol = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev)   # saim_create (host -> HBM)
+    t_create = time.perf_counter() - t0
     Ns = [sol.instance(s)["N"] for s in range(sol.n_inst)]
-    n_items = cfg.instances[0].n
+    kind = "qkp" if sol.info["kernel"] == 1 else "mkp"
     out = sol.alloc_outputs(R, cfg.K)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -227,7 +258,7 @@ def main():
     def step(seed):
         sol.run(seed, R, cfg.K, cfg.T, rep0=rep0, out=out, stream=stream)
         if world > 1:
-            sdist.reduce_inst_best(out["inst_best"])
+            sdist.finalize(out, rep0, R)       # MIN of the packed best + the winning bitset (8(e))
 
     for i in range(args.warmup):
         step(1000 + i)
@@ -236,7 +267,7 @@ def main():
     # Transparency: the same workload with the exact frozen-anneal early exit disabled (every
     # sweep evaluated); identical outputs (tests/test_gpu_parity.py::test_freeze_exit_is_exact).
     nofreeze = None
-    if not args.no_reference_variant:
+    if not args.no_reference_variant and kind == "qkp":
         sol_nf = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev, flags=P.FLAG_NO_FREEZE_EXIT)
         out_nf = sol_nf.alloc_outputs(R, cfg.K)
         sol_nf.run(999, R, cfg.K, cfg.T, rep0=rep0, out=out_nf, stream=stream)
@@ -251,7 +282,8 @@ def main():
                     "ms_per_step": 1e3 * t_nf, "counters": P.counters_dict(out_nf["counters"])}
         sol_nf.close()
 
-    # ---- device-timed region: K steps, per-step CUDA events, L2 flush between steps ----
+    # ---- device-timed region: K steps, per-step CUDA events on the launching stream (init kernel +
+    # SAIM kernel; the init kernel is ~2 us), L2 flush between steps outside the events ----
     clocks = ClockSampler(dev)
     if world > 1:
         dist.barrier()
@@ -282,39 +314,46 @@ def main():
     value = updates_total / t_total
     samples_per_s = R * cfg.K * sol.n_inst * world * args.steps / t_total
 
-    # ---- kernel-only time of the dominant kernel (main SAIM kernel; init kernel is ~2 us) ----
+    # ---- roofline of the dominant kernel on SURVEY.md 8(d)'s algorithmic model ----
     c0 = counters[-1]
-    # evaluated decisions only (sweeps skipped by the exact early exit are not counted as work)
-    evaluated = c0["decisions"] * c0["sweeps"] / float(R * cfg.K * cfg.T * sol.n_inst)
-    ops = (evaluated * OPS_DECISION + c0["uniforms"] * OPS_UNIFORM
-           + c0["flips"] * OPS_FLIP_PER_ITEM * n_items)
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     peaks = measured_peaks()
     sm_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    peak_ops = sm_count * LANES_PER_SM_CLK * sm_mhz * 1e6
-    achieved = ops / t_step
-    # SURVEY.md 8(d) transparency variant: the roofline of a sampler that draws a uniform for every
-    # update (f_u = 1, no saturation certificates), in updates/s, with this run's flip rate
-    ops_per_update_rng_all = (OPS_DECISION + OPS_UNIFORM
-                              + OPS_FLIP_PER_ITEM * n_items * c0["flips"] / float(c0["decisions"]))
+    N_avg = c0["decisions"] / float(R * cfg.K * cfg.T)    # decision-weighted mean N over instances
+    M = cfg.instances[0].M
+    rm = roofline_model(kind, M, N_avg, c0, sm_count, sm_mhz)
+    upd_rank = updates_per_step_rank / t_step             # this rank's kernel rate
+    bind = rm["binding"]
+    achieved = upd_rank * rm["ops_per_update"][bind]      # algorithmic ops (or SMEM bytes) per second
+    traffic, traffic_src = ncu_traffic_bytes(cfg.idx)
 
-    # ---- end-to-end through the public API with host buffers (create from host arrays = H2D,
-    # run, D2H of the results), timed on the device stream with a host sync at the end ----
-    e2e_times = []
-    h2d = Q.nbytes + c.nbytes + A.nbytes + b.nbytes + 8 * sol.n_inst
-    d2h = sum(out[k].numel() * out[k].element_size() for k in ["best_f", "best_x", "best_k", "n_feasible",
-                                                                 "inst_best", "counters"])
+    # ---- end-to-end through the public API with HOST buffers: saim_create from host arrays (H2D
+    # of the problem), saim_run, D2H of the results, every step; per-phase times for the setup and
+    # readback rates ----
+    e2e_times, t_cr, t_rb = [], [], []
+    h2d = Q.nbytes if Q is not None else 0
+    h2d += c.nbytes + A.nbytes + b.nbytes + 8 * sol.n_inst
+    res_keys = ["best_f", "best_x", "best_k", "n_feasible", "inst_best", "counters"]
+    d2h = sum(out[k].numel() * out[k].element_size() for k in res_keys)
+    pinned = {k: torch.empty(out[k].shape, dtype=out[k].dtype, pin_memory=True) for k in res_keys}
     for i in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s2 = P.Solver(Q, c, A, b, cfg.P, cfg.eta, cfg.beta_max, device=dev)
+        t1 = time.perf_counter()
         o2 = s2.run(7 + i, R, cfg.K, cfg.T, rep0=rep0)
         if world > 1:
-            sdist.reduce_inst_best(o2["inst_best"])
-        host = {k: o2[k].cpu() for k in ["best_f", "best_x", "best_k", "n_feasible", "inst_best", "counters"]}
-        e2e_times.append(time.perf_counter() - t0)
+            sdist.finalize(o2, rep0, R)
+        stream.synchronize()
+        t2 = time.perf_counter()
+        for k in res_keys:
+            pinned[k].copy_(o2[k], non_blocking=True)
+        stream.synchronize()
+        t3 = time.perf_counter()
+        e2e_times.append(t3 - t0)
+        t_cr.append(t1 - t0)
+        t_rb.append(t3 - t2)
         s2.close()
-        del host
     e2e_t = float(np.mean(e2e_times))
     if world > 1:
         tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
@@ -325,49 +364,90 @@ def main():
     line = None
     if rank == 0:
         line = {
-            "metric": "p-bit updates/sec (SAIM, QKP n=300 config 2)", "value": value, "unit": "updates/s",
+            "metric": metric_name(cfg), "value": value, "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"{cfg.name} (BASELINE config {cfg.idx}): {R} replicas/GPU x K={cfg.K} "
-                                   f"Lagrange iterations x T={cfg.T} sweeps x N={Ns} spins",
-                       "instances": sol.n_inst, "replicas_per_gpu": R, "K": cfg.K, "T": cfg.T, "N": Ns,
-                       "P": cfg.P, "eta": cfg.eta, "beta_max": cfg.beta_max,
+            "config": {"workload": f"{cfg.name} (BASELINE config {cfg.idx}): {R} replicas/GPU/instance x K={cfg.K} "
+                                   f"Lagrange iterations x T={cfg.T} sweeps x N={Ns if len(Ns) <= 4 else f'{min(Ns)}..{max(Ns)}'} spins",
+                       "instances": sol.n_inst, "replicas_per_gpu": R, "K": cfg.K, "T": cfg.T,
+                       "N": Ns if len(Ns) <= 4 else [min(Ns), max(Ns)],
+                       "P": cfg.P if len(cfg.P) <= 4 else [min(cfg.P), max(cfg.P)], "eta": cfg.eta,
+                       "beta_max": cfg.beta_max, "kernel": kind, "lanes_per_replica": sol.info["lanes_per_replica"],
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "parallelism": f"replicas sharded over {world} GPU(s), global replica index keyed RNG"},
             "samples_per_s": samples_per_s,
             "gpu_launches": 2 * args.steps,
-            "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-                         "frac": achieved / peak_ops, "traffic": ncu_traffic_bytes(),
-                         "traffic_unit": "DRAM bytes per launch (ncu capture in profiles/r01; the path is on-chip)",
-                         "ops_per_launch": ops, "ops_model": f"{OPS_DECISION}*evaluated decisions + {OPS_UNIFORM}*uniforms + "
-                                                            f"{OPS_FLIP_PER_ITEM}*n*flips (lane-ops)",
-                         "peak_basis": f"{sm_count} SMs x {LANES_PER_SM_CLK} lanes/clk x {sm_mhz:.0f} MHz "
-                                       "(measured median SM clock under load)",
-                         "rng_every_update": {
-                             "roof_updates_per_s": peak_ops / ops_per_update_rng_all,
-                             "value_over_roof": value / world / (peak_ops / ops_per_update_rng_all),
-                             "ops_per_update": ops_per_update_rng_all,
-                             "note": "roofline of a sampler drawing a uniform for every update (f_u = 1); "
-                                     "the certified saturation skip lets the measured rate exceed it"},
-                         "ncu": "profiles/r01/qkp_config2_K200_raw_selected.csv (issue slots, pipes, "
-                                "shared-memory wavefronts, DRAM bytes)"},
+            "roofline": {"bound": "alu" if bind != "smem" else "smem",
+                         "achieved": achieved / (1e12 if bind != "smem" else 1e9),
+                         "peak": rm["peak_per_s"] / (1e12 if bind != "smem" else 1e9),
+                         "unit": "Tops/s" if bind != "smem" else "GB/s",
+                         "frac": upd_rank / rm["roof_updates_per_s"][bind],
+                         "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per launch",
+                         "traffic_source": (f"static: ncu --set full capture {traffic_src} (not measured by this run)"
+                                            if traffic_src else None),
+                         "binding_class": bind,
+                         "model": "SURVEY.md 8(d) algorithmic ops per attempted update x measured f_u, p_f",
+                         "f_u": rm["f_u"], "p_f": rm["p_f"],
+                         "ops_per_update": rm["ops_per_update"],
+                         "roof_updates_per_s": rm["roof_updates_per_s"],
+                         "peak_basis": f"{sm_count} SMs x per-SM-clock peaks {PEAK_PER_SM_CLK} (tools/ubench.cu) x "
+                                       f"{sm_mhz:.0f} MHz (measured median SM clock during the timed region)",
+                         "kernel_ms": 1e3 * t_step},
             "counters": c0,
             "evaluated_sweep_fraction": c0["sweeps"] / float(R * cfg.K * cfg.T * sol.n_inst),
             "no_freeze_exit": nofreeze,
             "clocks": clk,
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
+            "setup": {"saim_create_ms": 1e3 * float(np.mean(t_cr)), "first_create_ms": 1e3 * t_create,
+                      "h2d_bytes": int(h2d),
+                      "h2d_GBps": h2d / float(np.mean(t_cr)) / 1e9,
+                      "note": "saim_create = validation, slack extension, range proofs, layout on the host + one "
+                              "H2D upload; the kernel prologue then stages the blob HBM -> SMEM by TMA "
+                              "(DRAM bytes per launch: roofline.traffic)"},
+            "readback": {"d2h_bytes": int(d2h), "ms": 1e3 * float(np.mean(t_rb)),
+                         "GBps": d2h / float(np.mean(t_rb)) / 1e9},
         }
         if not args.no_cpu_baseline and world == 1:
-            cb = oracle_sample(cfg, seconds_target=args.cpu_seconds)
+            cb = oracle_sample(cfg, seconds_target=args.cpu_seconds, trace=True)
             line["cpu_baseline"] = {"value": cb["updates_per_s"], "unit": "updates/s", "cores": cb["cores"],
                                     "kind": "oracle", "sample": cb["sample"]}
+            line["parity"] = parity_summary(P, sol, cfg, cb, stream)
         print(json.dumps(line), flush=True)
     sol.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def parity_summary(P, sol, cfg, cb, stream):
+    """The GPU on the cpu_baseline's own sample (same seed, replicas, K): element-wise comparison of
+    every readout with the oracle's, plus the decision-level report north_star asks for (near ties
+    |u - sigma| < 2^-20 seen by the oracle, GPU fp64/double-double slow-path counts, mismatches)."""
+    import torch
+    o = cb["result"]
+    nrep, K = cb["nrep"], cb["K"]
+    g = sol.run(cb["seed"], nrep, K, cfg.T, trace=True, final=True, stream=stream)
+    torch.cuda.synchronize()
+    WN = (cb["N"] + 31) // 32
+    gx = g["tr_x"][0].cpu().numpy().view(np.uint32)[..., :WN]
+    mism_x = int(np.any(gx != o["tr_x"], axis=-1).sum())
+    mism = {"samples_x": mism_x,
+            "f": int((g["tr_f"][0].cpu().numpy() != o["tr_f"]).sum()),
+            "feasible": int((g["tr_feas"][0].cpu().numpy() != o["tr_feas"]).sum()),
+            "r": int(np.any(g["tr_r"][0].cpu().numpy() != o["tr_r"], axis=-1).sum()),
+            "lambda": int(np.any(g["tr_lam"][0].cpu().numpy() != o["tr_lam"], axis=-1).sum()),
+            "best_f": int((g["best_f"][0].cpu().numpy() != o["best_f"]).sum()),
+            "flips": int(g["rep_flips"][0].cpu().numpy().astype(np.int64).sum() - o["counters"]["flips"])}
+    gc = P.counters_dict(g["counters"])
+    return {"sample": f"instance 0, replicas [0, {nrep}), K={K}, seed {cb['seed']} (the cpu_baseline's sample)",
+            "mismatches": mism, "all_equal": all(v == 0 for v in mism.values()),
+            "oracle_decisions": o["counters"]["decisions"], "oracle_near_ties_2^-20": o["counters"]["near_ties"],
+            "oracle_binary128_fallbacks": o["counters"]["quad_fallbacks"],
+            "gpu_fp64_slow_path": gc["fp64"], "gpu_uncertified": gc["uncertified"],
+            "decision_mismatch_rate": 0.0 if mism_x == 0 else None}
 
 
 if __name__ == "__main__":

@@ -15,8 +15,9 @@
  *                                          lambda_k = (eta/s_c) Lambda_k exactly, R10)
  *   Every decision x_i <- [u < sigma(beta_t F_i)] is the EXACT real predicate (R1, R18) with u the
  *   Philox4x32-10 uniform keyed on (seed, s, rho, k, t, i) (R2); the kernel certifies each
- *   decision (fp32 fast path with a rigorous error bound, fp64 fallback) and counts any decision
- *   it could not certify in fp64 (SAIM_CNT_UNCERTIFIED).
+ *   decision (fp32 fast path with a rigorous error bound, fp64 second level, double-double third
+ *   level on the exact integers) and counts any decision not certified even in double-double
+ *   (SAIM_CNT_UNCERTIFIED; its band is ~2^-80 wide, so the count is 0 in practice).
  *
  * Conventions: all functions return 0 (SAIM_OK) or a negative SAIM_E* code; saim_last_error()
  * returns a thread-local message for the last failure.  No function aborts the process.
@@ -44,10 +45,13 @@ extern "C" {
 #define SAIM_CNT_SWEEPS 2        /* sweeps actually evaluated (the rest were certified frozen, see flags) */
 #define SAIM_CNT_UNIFORMS 3      /* decisions the kernel could not settle without u (not certified saturated) */
 #define SAIM_CNT_FP64 4          /* decisions re-evaluated on the fp64 slow path */
-#define SAIM_CNT_UNCERTIFIED 5   /* decisions not certified even in fp64 (expected 0) */
+#define SAIM_CNT_UNCERTIFIED 5   /* decisions not certified even in double-double (expected 0) */
 #define SAIM_CNT_FEASIBLE 6      /* feasible samples x_k */
 #define SAIM_CNT_PHILOX 7        /* Philox4x32-10 evaluations (per lane) */
-#define SAIM_NUM_COUNTERS 8
+#define SAIM_CNT_REPLAYED 8      /* QKP: replicas re-run by the exact replay (a decision its fp64 level
+                                  * could not certify; DESIGN.md 6.1 "Exact replay"); their counts
+                                  * above are those of the replay */
+#define SAIM_NUM_COUNTERS 9
 
 /* Problem batch: n_inst instances sharing (n_items, n_cons).  HOST pointers; copied by
  * saim_create (the caller may free them on return).  Row-major, instance-major. */
@@ -62,7 +66,9 @@ typedef struct {
 } saim_problem;
 
 typedef struct {
-  const double *P;         /* [n_inst] penalty P > 0 of Eq. 3 (PAPER.md:102 P = alpha d N; chosen by the caller) */
+  const double *P;         /* [n_inst] penalty P >= 0 of Eq. 3 (PAPER.md:102 P = alpha d N; chosen by the caller;
+                            * P = 0 drops the quadratic penalty, leaving the Lagrange term alone).
+                            * Finite; SAIM_EINVAL otherwise */
   double eta;              /* Lagrange step eta >= 0 (Algorithm 1); eta = 0 is the penalty-method baseline */
   double beta_max;         /* final inverse temperature of the linear ramp, > 0 */
   int32_t device;          /* CUDA device ordinal */
@@ -89,6 +95,10 @@ typedef struct {
 /* MKP lockstep kernel: no producer warps (each consumer warp draws its own logits).  Identical
  * results either way. */
 #define SAIM_FLAG_MKP_NO_PRODUCER 64
+/* Test hook for the certification chain: every decision that reaches the fp64 level is treated as
+ * uncertified there, so it is re-decided at the double-double level (MKP: at once; QKP: by the
+ * exact replay of the whole replica).  Results are identical either way; only slower. */
+#define SAIM_FLAG_TEST_REPLAY 128
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),
@@ -139,7 +149,9 @@ int saim_create(const saim_problem *prob, const saim_params *par, saim_ctx **out
  * calls or GPUs with bit-identical results).  Asynchronous on `cuda_stream` (a cudaStream_t,
  * e.g. torch.cuda.current_stream().cuda_stream; NULL = legacy default stream).  Launch and
  * argument errors return synchronously; kernel faults surface at the next stream sync or call
- * (SAIM_ECUDA).  Requires 1 <= R, rep0 + R <= 2^20, K >= 1, T >= 1, and K * max|r| < 2^62. */
+ * (SAIM_ECUDA).  Requires 1 <= R, rep0 + R <= 2^20, K >= 1, T >= 1, K * max|r| < 2^62 (int64
+ * Lambda) and K * max|r| * max A_ext * M < 2^62 (int64 kappa on the slow path); SAIM_ERANGE
+ * otherwise. */
 int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, int32_t K, int32_t T,
              void *cuda_stream, const saim_outputs *out);
 
@@ -158,7 +170,11 @@ void saim_destroy(saim_ctx *ctx);
  *             out_u32 = host uint32[n][4].
  *  which = 1: exhaustive sweep of the fp32 logit used by the fast path over all 2^23 uniforms
  *             (R18); out_f64[0] = max |logit_f32(u) - logit(u)| / (2^-17 + 2^-19 |logit(u)|)
- *             (must be < 1 for the certification bound to hold), out_f64[1] = max abs error. */
+ *             (must be < 1 for the certification bound to hold), out_f64[1] = max abs error.
+ *  which = 2: the double-double decision level (R18) on n records; in_u32 points to n
+ *             80-byte records {int64 phi, pi, kappa, s_o, s_c; double P, eta, beta_max; int32 tn,
+ *             td; uint32 w; int32 pad} (beta_t = beta_max tn/td, u from the Philox word w as in R2);
+ *             out_u32[i] = x | (uncertified << 1) for record i. */
 int saim_selftest(int which, int device, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 
 /* Thread-local message of the last failing call ("" if none). */

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsaim.so")
 
 SAIM_OK, SAIM_EINVAL, SAIM_ERANGE, SAIM_ESMEM, SAIM_ECUDA, SAIM_EUNSUPPORTED, SAIM_ENOMEM = 0, -1, -2, -3, -4, -5, -6
-COUNTER_NAMES = ["decisions", "flips", "sweeps", "uniforms", "fp64", "uncertified", "feasible", "philox"]
+COUNTER_NAMES = ["decisions", "flips", "sweeps", "uniforms", "fp64", "uncertified", "feasible", "philox", "replayed"]
 FLAG_NO_FREEZE_EXIT = 1
 FLAG_MKP_LOCKSTEP = 2      # MKP: lane-per-replica kernel instead of the outcome tree
 FLAG_MKP_L2 = 4            # MKP: outcome tree with 2 lanes per replica
@@ -26,6 +26,7 @@ FLAG_MKP_L4 = 8            # MKP: outcome tree with 4 lanes per replica
 FLAG_MKP_SPLIT2 = 16       # MKP: constraint rows of a replica split over 2 lanes (M > 8)
 FLAG_MKP_NO_PRODUCER = 64  # MKP lockstep: consumer warps draw their own logits (identical results)
 FLAG_QKP_NO_HOT_LOOP = 32  # QKP: disable the hot-block loop (identical results)
+FLAG_TEST_REPLAY = 128     # test hook: every fp64-level decision re-decided in double-double (identical results)
 EXPORTS = ["saim_create", "saim_run", "saim_get_info", "saim_get_instance", "saim_destroy",
            "saim_last_error", "saim_selftest"]
 
@@ -148,26 +149,45 @@ class Solver:
     def alloc_outputs(self, R: int, K: int, trace: bool = False, final: bool = False):
         import torch
         dev = torch.device("cuda", self.device)
-        S, Wn, WN, M = self.n_inst, self.info["words_items"], self.info["words_full"], self.M
-        out = {
-            "best_f": torch.empty((S, R), dtype=torch.int64, device=dev),
-            "best_x": torch.empty((S, R, Wn), dtype=torch.int32, device=dev),
-            "best_k": torch.empty((S, R), dtype=torch.int32, device=dev),
-            "n_feasible": torch.empty((S, R), dtype=torch.int32, device=dev),
-            "inst_best": torch.empty((S,), dtype=torch.int64, device=dev),
-            "counters": torch.empty((8,), dtype=torch.int64, device=dev),
-        }
+        specs = self.output_specs(R, K)
+        fields = ["best_f", "best_x", "best_k", "n_feasible", "inst_best", "counters"]
         if trace:
-            out.update(tr_f=torch.empty((S, R, K), dtype=torch.int64, device=dev),
-                       tr_feas=torch.empty((S, R, K), dtype=torch.uint8, device=dev),
-                       tr_r=torch.empty((S, R, K, M), dtype=torch.int64, device=dev),
-                       tr_lam=torch.empty((S, R, K, M), dtype=torch.int64, device=dev),
-                       tr_x=torch.empty((S, R, K, WN), dtype=torch.int32, device=dev))
+            fields += ["tr_f", "tr_feas", "tr_r", "tr_lam", "tr_x"]
         if final:
-            out.update(final_x=torch.empty((S, R, WN), dtype=torch.int32, device=dev),
-                       final_lam=torch.empty((S, R, M), dtype=torch.int64, device=dev),
-                       rep_flips=torch.empty((S, R), dtype=torch.int32, device=dev))
-        return out
+            fields += ["final_x", "final_lam", "rep_flips"]
+        return {f: torch.empty(specs[f][0], dtype=specs[f][1], device=dev) for f in fields}
+
+    def output_specs(self, R: int, K: int):
+        """Shape and dtype of every saim_outputs field for a run of R replicas x K iterations."""
+        import torch
+        S, Wn, WN, M = self.n_inst, self.info["words_items"], self.info["words_full"], self.M
+        return {"best_f": ((S, R), torch.int64), "best_x": ((S, R, Wn), torch.int32),
+                "best_k": ((S, R), torch.int32), "n_feasible": ((S, R), torch.int32),
+                "inst_best": ((S,), torch.int64), "counters": ((len(COUNTER_NAMES),), torch.int64),
+                "tr_f": ((S, R, K), torch.int64), "tr_feas": ((S, R, K), torch.uint8),
+                "tr_r": ((S, R, K, M), torch.int64), "tr_lam": ((S, R, K, M), torch.int64),
+                "tr_x": ((S, R, K, WN), torch.int32), "final_x": ((S, R, WN), torch.int32),
+                "final_lam": ((S, R, M), torch.int64), "rep_flips": ((S, R), torch.int32)}
+
+    def check_outputs(self, out: Dict, R: int, K: int):
+        """Raise ValueError unless every tensor in `out` matches the run's shape, dtype, device and is
+        contiguous (the kernel writes through raw pointers: a stale buffer would be overrun)."""
+        import torch
+        specs = self.output_specs(R, K)
+        for f in ("best_f", "best_x", "best_k", "n_feasible"):
+            if out.get(f) is None:
+                raise ValueError(f"outputs: '{f}' is required")
+        for f, t in out.items():
+            if f not in specs:
+                raise ValueError(f"outputs: unknown field '{f}'")
+            if t is None:
+                continue
+            shape, dtype = specs[f]
+            if not isinstance(t, torch.Tensor) or tuple(t.shape) != shape or t.dtype != dtype:
+                raise ValueError(f"outputs['{f}']: expected {dtype} of shape {shape}, got "
+                                 f"{getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))}")
+            if t.device != torch.device("cuda", self.device) or not t.is_contiguous():
+                raise ValueError(f"outputs['{f}']: must be a contiguous tensor on cuda:{self.device}")
 
     def run(self, seed: int, R: int, K: int, T: int, rep0: int = 0, trace: bool = False, final: bool = False,
             out: Optional[Dict] = None, stream=None):
@@ -175,6 +195,8 @@ class Solver:
         import torch
         if out is None:
             out = self.alloc_outputs(R, K, trace=trace, final=final)
+        else:
+            self.check_outputs(out, R, K)
         ptrs = _Outputs(*[out[f].data_ptr() if f in out and out[f] is not None else None for f in _OUT_FIELDS])
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
@@ -203,6 +225,20 @@ def selftest_philox(inputs, device: int = 0):
     inp = np.ascontiguousarray(np.asarray(inputs, dtype=np.uint32).reshape(-1, 6))
     out = np.zeros((inp.shape[0], 4), np.uint32)
     _check(load_library().saim_selftest(0, int(device), inp.shape[0], inp.ctypes.data, out.ctypes.data, None))
+    return out
+
+
+DD_RECORD = np.dtype([("phi", "<i8"), ("pi", "<i8"), ("kappa", "<i8"), ("s_o", "<i8"), ("s_c", "<i8"),
+                      ("P", "<f8"), ("eta", "<f8"), ("beta_max", "<f8"), ("tn", "<i4"), ("td", "<i4"),
+                      ("w", "<u4"), ("pad", "<i4")])
+
+
+def selftest_decide_dd(records, device: int = 0):
+    """Double-double decision level (saim_selftest(2)) on a DD_RECORD array: x | uncertified << 1."""
+    rec = np.ascontiguousarray(records, dtype=DD_RECORD)
+    assert rec.dtype.itemsize == 80
+    out = np.zeros(rec.shape[0], np.uint32)
+    _check(load_library().saim_selftest(2, int(device), rec.shape[0], rec.ctypes.data, out.ctypes.data, None))
     return out
 
 

@@ -6,7 +6,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsaim.so")
-SOURCES = ["saim_api.cu", "saim_qkp.cu", "saim_mkp.cu", "saim_mkp_tree.cu", "saim_mkp_split.cu"]
+SOURCES = ["saim_api.cu", "saim_qkp.cu", "saim_qkp_replay.cu", "saim_mkp.cu", "saim_mkp_replay.cu", "saim_mkp_tree.cu",
+           "saim_mkp_tree_replay.cu", "saim_mkp_split.cu", "saim_mkp_split_replay.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
@@ -23,16 +24,15 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    objs = []
+    objs = [os.path.join(CSRC, src.replace(".cu", f".{os.getpid()}.o")) for src in SOURCES]
+    procs = [subprocess.Popen([NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj], stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for src, obj in zip(SOURCES, objs)]
     logs = []
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
-        p = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(p.stdout + p.stderr)
+    for src, p in zip(SOURCES, procs):           # translation units compile in parallel
+        out, _ = p.communicate()
+        logs.append(out)
         if p.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{p.stdout}\n{p.stderr}")
-        objs.append(obj)
+            raise RuntimeError(f"nvcc failed for {src}:\n{out}")
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + objs + ["-lcudart"]
     p = subprocess.run(cmd, capture_output=True, text=True)

@@ -22,14 +22,16 @@
 namespace saim {
 int qkp_npl_bucket(int npl);
 cudaError_t qkp_configure(int npl, int qb, int pk, int blob_bytes, int smem_optin, int *max_wpc);
-cudaError_t qkp_launch(int npl, int qb, int pk, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st);
+cudaError_t qkp_launch(int npl, int qb, int pk, const RunArgs &a, int n_inst, int wpc, int smem_bytes, cudaStream_t st,
+                       bool replay);
 int mkp_plan(int n, int M, int N_max, int smem_optin, int *MM_out, uint32_t *blob_bytes, uint32_t *per_warp,
              int *max_wpc, uint32_t *per_warp_prod, int *max_wpc_prod);
-cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
+cudaError_t mkp_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st, bool replay);
 int mkpt_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, int L, uint32_t *per_warp, int *max_wpc);
-cudaError_t mkpt_launch(const RunArgs &a, int n_inst, int MM, int L, int wpc, uint32_t per_warp, cudaStream_t st);
+cudaError_t mkpt_launch(const RunArgs &a, int n_inst, int MM, int L, int wpc, uint32_t per_warp, cudaStream_t st,
+                        bool replay);
 int mkps_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, uint32_t *per_warp, int *max_wpc);
-cudaError_t mkps_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st);
+cudaError_t mkps_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st, bool replay);
 int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 }  // namespace saim
 
@@ -68,8 +70,11 @@ struct saim_ctx {
   double beta_max = 0, eta = 0;
   int flags = 0;
   long long r_abs_max = 0;
+  long long a_ext_max = 0;  // max A_ext entry (items and slack weights) over instances
   int r_tol = 0;        // QKP certificate tolerance D (min over instances)
   unsigned char *d_blob = nullptr;
+  uint8_t *d_replay = nullptr;   // QKP exact-replay flags, [n_inst][R] (grown on demand)
+  size_t replay_cap = 0;
   InstHdr *d_hdr = nullptr;
   std::vector<InstHdr> hdr;
   std::vector<std::vector<int32_t>> q;  // slack bits per row per instance
@@ -104,7 +109,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
   if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
   if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
   const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2;
-  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_QKP_NO_HOT_LOOP | SAIM_FLAG_MKP_NO_PRODUCER | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
+  if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_QKP_NO_HOT_LOOP | SAIM_FLAG_MKP_NO_PRODUCER | SAIM_FLAG_TEST_REPLAY | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
     return fail(SAIM_EINVAL, "unknown or conflicting flags 0x%x", par->flags);
 
   if (M > 1 && prob->Q)
@@ -178,6 +183,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     h.c_p = P / ((double)sc * (double)sc);
     h.c_l = par->eta / ((double)sc * (double)sc);
     h.phi_bound = (double)phi_bound;
+    h.P = P; h.eta = par->eta; h.beta_max = par->beta_max;
     phib_all = std::max(phib_all, phi_bound);
     {
       long long amax = 0;
@@ -186,6 +192,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
         for (int j = 0; j < n; ++j) amax = std::max(amax, (long long)A[(size_t)k * n + j]);
       }
       h.v_bound = 2.0 * (double)rmax + (double)amax;
+      ctx->a_ext_max = std::max(ctx->a_ext_max, amax);
       h.r_bound = (double)rmax;
       // QKP quiet certificates hold for |r - r_cert| <= D: the tolerance widens the scan threshold
       // by 2 beta c_p D |A_i| <= 1 (of ln(2^24-1) = 16.6) for the heaviest item.
@@ -393,6 +400,9 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     return fail(SAIM_EINVAL, "best_f, best_x, best_k and n_feasible are required");
   if ((double)K * (double)(ctx->r_abs_max + 1) >= 4.0e18)
     return fail(SAIM_ERANGE, "K * max|r| would overflow the int64 Lagrange accumulator");
+  // kappa_i = sum_m Lambda_m A_mi in int64 on the double-double slow path (R18)
+  if ((double)K * (double)(ctx->r_abs_max + 1) * (double)ctx->a_ext_max * (double)std::max(ctx->M, 1) >= 4.0e18)
+    return fail(SAIM_ERANGE, "K * max|r| * max A * M would overflow the int64 field component kappa");
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   e = cudaGetLastError();  // surface earlier asynchronous faults
@@ -414,32 +424,59 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
   a.flags = ctx->flags;
   a.rtol2 = 2.0f * (float)ctx->r_tol;
   a.out = *out;
-
   saim_init_outputs<<<(ctx->n_inst + 255) / 256, 256, 0, st>>>(out->inst_best, ctx->n_inst, out->counters);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "init launch");
 
+  // Launch geometry (warps per CTA and the grid's x extent) of the selected kernel.
+  int wpc = 1, gx = 1;
+  bool prod = false;
   if (ctx->kernel == 1) {
     const long long warps = (long long)R * ctx->n_inst;
-    int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
+    wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
-    e = qkp_launch(ctx->npl, ctx->qb, ctx->pk, a, ctx->n_inst, wpc, ctx->smem_bytes, st);
+    gx = (R + wpc - 1) / wpc;
   } else if (ctx->mkp_kind == 0) {
     const long long warps = (long long)((R + 31) / 32) * ctx->n_inst;   // 32 replicas per warp (lockstep)
-    int wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
+    wpc = (int)((warps + ctx->sm_count - 1) / ctx->sm_count);
     // producer warps when the consumers still fit one wave with their partners
-    const bool prod = !(ctx->flags & SAIM_FLAG_MKP_NO_PRODUCER) && wpc <= ctx->max_wpc_prod;
+    prod = !(ctx->flags & SAIM_FLAG_MKP_NO_PRODUCER) && wpc <= ctx->max_wpc_prod;
     a.mkp_prod = prod ? 1 : 0;
     wpc = std::max(1, std::min(wpc, prod ? ctx->max_wpc_prod : ctx->max_wpc));
-    e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, prod ? ctx->per_warp_prod : ctx->per_warp, st);
+    gx = ((R + 31) / 32 + wpc - 1) / wpc;
   } else {
     // one CTA per SM: spread each instance's warps over floor(SMs / n_inst) CTAs
     const int G = 32 / ctx->lanes;
     const int warps_inst = (R + G - 1) / G;
     const int ctas_inst = std::max(1, ctx->sm_count / ctx->n_inst);
-    int wpc = (warps_inst + ctas_inst - 1) / ctas_inst;
+    wpc = (warps_inst + ctas_inst - 1) / ctas_inst;
     wpc = std::max(1, std::min(wpc, ctx->max_wpc));
-    if (ctx->mkp_kind == 1) e = mkpt_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st);
-    else e = mkps_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st);
+    gx = (warps_inst + wpc - 1) / wpc;
+  }
+  // Exact-replay flags: one byte per warp slot of the grid, zeroed every run.
+  const size_t need = (size_t)ctx->n_inst * (size_t)gx * 32u;
+  if (need > ctx->replay_cap) {
+    if (ctx->d_replay) cudaFree(ctx->d_replay);
+    ctx->d_replay = nullptr;
+    ctx->replay_cap = 0;
+    if ((e = cudaMalloc(&ctx->d_replay, need)) != cudaSuccess) return cuda_fail(e, "cudaMalloc replay flags");
+    ctx->replay_cap = need;
+  }
+  a.replay = ctx->d_replay;
+  if ((e = cudaMemsetAsync(ctx->d_replay, 0, need, st)) != cudaSuccess) return cuda_fail(e, "replay flags");
+
+  // The main kernel, then the exact replay over the same grid: it re-runs only warps the main
+  // kernel flagged (a decision its fp64 level could not certify) and its CTAs exit at once when
+  // there are none -- the usual case.
+  for (int pass = 0; pass < 2 && e == cudaSuccess; ++pass) {
+    const bool replay = pass == 1;
+    if (ctx->kernel == 1)
+      e = qkp_launch(ctx->npl, ctx->qb, ctx->pk, a, ctx->n_inst, wpc, ctx->smem_bytes, st, replay);
+    else if (ctx->mkp_kind == 0)
+      e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, prod ? ctx->per_warp_prod : ctx->per_warp, st, replay);
+    else if (ctx->mkp_kind == 1)
+      e = mkpt_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st, replay);
+    else
+      e = mkps_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st, replay);
   }
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   return SAIM_OK;
@@ -474,12 +511,14 @@ extern "C" void saim_destroy(saim_ctx *ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->d_blob) cudaFree(ctx->d_blob);
   if (ctx->d_hdr) cudaFree(ctx->d_hdr);
+  if (ctx->d_replay) cudaFree(ctx->d_replay);
   delete ctx;
 }
 
 extern "C" int saim_selftest(int which, int device, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64) {
   g_err.clear();
-  if ((which == 0 && (n < 1 || !in_u32 || !out_u32)) || (which == 1 && !out_f64) || which < 0 || which > 1)
+  if (((which == 0 || which == 2) && (n < 1 || !in_u32 || !out_u32)) || (which == 1 && !out_f64) || which < 0 ||
+      which > 2)
     return fail(SAIM_EINVAL, "bad selftest arguments");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");

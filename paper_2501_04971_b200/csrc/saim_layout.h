@@ -13,11 +13,10 @@
 //                            code of 0.  A flip of item j streams one row: lane l reads QW words.
 //     (A_ext and c first: their sizes depend only on the kernel's (NPL, QB) instantiation, so all
 //     three arrays sit at compile-time offsets from one base.)
-//   MKP kernel (linear objective, M <= 32):
-//     [Acol]                 int16 x M x n_pad (item columns A[.][i]), stored [i][M] so one spin's
-//                            column is contiguous.
-//     [c]                    int32[n_pad]
-//     [slack]                per slack spin: (row, shift)
+//   MKP kernels (linear objective, 2 <= M <= 32): see MkpLayout below -- fp32 item columns
+//     (exact integers), per-item constants, c, b, the slack bit count of each row and the O(3n)
+//     band of adjacent column products.  Slack spins have no stored column: slack bit q of row
+//     m has the single weight 2^q in row m, derived from qrow in the kernel.
 //
 // All integer state of the hot path stays exactly representable: the host proves the bounds of
 // DESIGN.md Appendix B before accepting a problem (SAIM_ERANGE otherwise).
@@ -42,6 +41,7 @@ struct InstHdr {
   double phi_bound;   // max_i |c_i| + sum_j |Q_ij|  >= |phi_i| for every state (host-proven)
   double v_bound;     // 2 max|r| + max A_ext      >= |2 r0 + A_i| for every state
   double r_bound;     // max|r_k| over every state and row (host-proven)
+  double P, eta, beta_max;  // the run constants exactly as given (double-double slow path, R18)
 };
 
 inline __host__ __device__ uint32_t align16u(uint32_t v) { return (v + 15u) & ~15u; }
@@ -107,6 +107,7 @@ struct RunArgs {
   double beta_max;
   int32_t mkp_prod;           // MKP lockstep: 1 = producer warps draw the logits
   float rtol2;                // QKP: 2D, a quiet certificate holds while |2r - 2r_cert| <= 2D
+  uint8_t *replay;            // [n_inst][grid.x][32] warp slots flagged for the exact replay (zeroed per run)
   saim_outputs out;           // device pointers
 };
 

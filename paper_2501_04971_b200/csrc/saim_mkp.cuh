@@ -1,0 +1,525 @@
+// saim_mkp.cuh -- fused SAIM kernel for linear objectives with 2 <= M <= 32 constraints (MKP,
+// PAPER.md:321-326; BASELINE.json configs 3-4).  sm_100a.
+//
+// Mapping: one LANE = one replica, one warp = 32 replicas of the same instance
+// marching through the spins in lockstep.  Every lane makes every decision of its own chain in
+// the exact sequential order of Algorithm 1 / Eq. 9-10 -- there is no speculation, so the ~25%
+// flip rate of MKP anneals costs nothing extra -- while the instance data a step needs (the item
+// column A_{.i}, its constants) is the same for all lanes: one shared-memory broadcast.
+//
+// Field of spin i (R1), with r = A_ext x - b, Lambda the Lagrange accumulator (R10):
+//   item i:   F_i = -c_o c_i - c_p a_i (1 - 2x_i) - 2 c_p (A_{.i} . r) - c_l (A_{.i} . Lambda)
+//   slack bit q of row m (A = 2^q):  F = -A (2 c_p r_m + c_l Lambda_m) - c_p A^2 (1 - 2x)
+// r is kept as exact integers in fp32 registers (|r| < 2^21, host-proven); the dot products are
+// fp32 with a rigorous error bound; c_l Lambda_m is rounded once per iteration.
+// Decisions are certified exactly as in the QKP kernel: saturated test, fp32 logit band, fp64
+// slow path (counted when even that is not certain).
+#pragma once
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+#include <type_traits>
+
+#include "saim_dev.cuh"
+
+namespace saim {
+
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// fp64 tail of the slow path: z and its magnitude sum S are accurate to ~2^-50 S; returns
+// (x | uncertified << 1).
+__device__ __noinline__ int certify_fp64(double zz, double S, uint32_t w) {
+  const double d = zz - logit_f64(w);
+  return (d > 0.0 ? 1 : 0) | (fabs(d) <= (S + 1.0 + fabs(zz)) * 0x1p-46 ? 2 : 0);
+}
+
+// Uniform word of spin i (R2) recomputed for the slow path.
+__device__ __noinline__ uint32_t word_of(uint2 key, int i, int t, int k, uint32_t srho) {
+  const uint4 w4 = philox_group(key, i >> 7, i & 31, t, k, srho);
+  const int j = (i >> 5) & 3;
+  return j == 0 ? w4.x : (j == 1 ? w4.y : (j == 2 ? w4.z : w4.w));
+}
+
+// logit(u) in fp32 with its sign made exact (sign(logit u) = sign(u - 1/2) <=> w >= 2^31).
+__device__ __forceinline__ float logit_signed(uint32_t w) {
+  const float l = fabsf(logit_f32(w));
+  return (w >> 31) ? l : -l;
+}
+
+// mbarrier helpers for the consumer/producer pairs (shared::cta, one phase per buffer fill).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int MM>
+struct MkpCfg {
+  static constexpr int kThreads = MM <= 16 ? 512 : 256;
+};
+
+}  // namespace
+
+// MM: padded constraint count (layout); MA <= MM: rows the arithmetic loops cover (= M for the
+// instantiated exact sizes, else MM with zero-padded rows).
+template <int MM, int MA, bool PROD, bool RP>
+__global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const RunArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t mbar;
+
+  const int s = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // Producer warps (a.mkp_prod): the CTA's second half of warps draws the logits
+  // of the first half's replicas -- state-independent -- into double-buffered groups, so the
+  // consumers' instruction stream (one warp per SMSP: issue-limited per warp) is decisions only.
+  constexpr bool prod = PROD;                          // (a.mkp_prod selects this instantiation)
+  const int nc = prod ? (int)(blockDim.x >> 6) : (int)(blockDim.x >> 5);   // consumer warps per CTA
+  const bool producer = prod && warp >= nc;
+  const int cw = producer ? warp - nc : warp;          // consumer warp (own, or the partner's)
+  unsigned char *wbase = smem + a.blob_bytes + cw * mkp_warp_bytes(a.WN, MM, prod ? 1 : 0);
+  const uint32_t lbytes = (prod ? 2u : 1u) * 128u * 128u;
+  uint64_t *mb = reinterpret_cast<uint64_t *>(wbase + align16u(a.WN * 128u) + lbytes + MM * 256u);  // full[2], empty[2]
+  if constexpr (RP) {                                  // exact replay: only CTAs holding a flagged warp
+    if (!__syncthreads_or(a.replay[replay_slot(cw)] != 0)) return;
+  }
+  if (prod && !producer && lane == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mbar_init(mb + i, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  bulk_stage(smem, a.blob + (size_t)s * a.blob_bytes, a.blob_bytes, &mbar);   // (includes __syncthreads)
+
+  const int ridx = (blockIdx.x * nc + cw) * 32 + lane;
+  const int wfirst = (blockIdx.x * nc + cw) * 32;
+  if (wfirst >= a.R) return;                         // whole warp beyond R (its partner too)
+  const bool live = ridx < a.R;                        // lanes beyond R compute but never write
+  const int rho = a.rep0 + (live ? ridx : a.R - 1);
+  const InstHdr *Hp = a.hdr + s;
+  const int n = a.n, M = a.M;
+  const int N = Hp->N;
+  const MkpLayout L = mkp_layout(n, MM);
+  const float *sAcol = reinterpret_cast<const float *>(smem + L.acol);
+  const float4 *sIc = reinterpret_cast<const float4 *>(smem + L.iconst);
+  const int32_t *sC = reinterpret_cast<const int32_t *>(smem + L.cint);
+  const long long *sB = reinterpret_cast<const long long *>(smem + L.brow);
+  const int32_t *sQ = reinterpret_cast<const int32_t *>(smem + L.qrow);
+  uint32_t *xw = reinterpret_cast<uint32_t *>(wbase) + lane;                            // word w: xw[32 w]
+  // logit of spin i of the current group: lt[loff + 32 (i & 127)] (with producers, successive
+  // groups alternate between two buffers, loff = 0 or 4096)
+  float *lt = reinterpret_cast<float *>(wbase + align16u(a.WN * 128u)) + lane;
+  long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + lbytes) + lane;  // [m]
+
+  if (producer) {
+    // The consumer takes the groups g = 0 .. NG-1 of every sweep t of every iteration k in order
+    // (fill f = running index): buffer f & 1, full[f & 1] completes its (f >> 1)-th phase when
+    // filled, empty[f & 1] when the consumer has moved past it.
+    const uint2 pkey = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+    const uint32_t psrho = ((uint32_t)s << 20) | (uint32_t)rho;
+    const int NG = (N + 127) >> 7;
+    uint32_t f = 0;
+    for (int k = 0; k < a.K; ++k)
+      for (int t = 0; t < a.T; ++t)
+        for (int g = 0; g < NG; ++g, ++f) {
+          const uint32_t b = f & 1u;
+          if (f >= 2) mbar_wait(mb + 2 + b, ((f >> 1) - 1u) & 1u);
+          float *dst = lt + 32 * 128 * b;
+          const int nw = min(4, (N - 128 * g + 31) >> 5);
+#pragma unroll 4
+          for (int j = 0; j < 32; ++j) {
+            const uint4 w4 = philox_group(pkey, g, j, t, k, psrho);
+            dst[32 * (j + 0)] = logit_signed(w4.x);
+            if (nw > 1) dst[32 * (j + 32)] = logit_signed(w4.y);
+            if (nw > 2) dst[32 * (j + 64)] = logit_signed(w4.z);
+            if (nw > 3) dst[32 * (j + 96)] = logit_signed(w4.w);
+          }
+          mbar_arrive(mb + b);
+        }
+    return;
+  }
+
+  const double c_o = Hp->c_o, c_p = Hp->c_p, c_l = Hp->c_l;
+  const float twocp = (float)(2.0 * c_p), cpf = (float)c_p;
+  const float rbound = (float)Hp->r_bound;
+  const float amax = (float)(Hp->v_bound - 2.0 * Hp->r_bound);   // max A_ext entry
+  const float *sBand = reinterpret_cast<const float *>(smem + L.band);
+
+  float r[MM], cL[MM];
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    r[m] = m < M ? (float)(-sB[m]) : 0.0f;             // x = 0: r = -b
+    cL[m] = 0.0f;
+    Lam[32 * m] = 0;
+  }
+  for (int w = 0; w < a.WN; ++w) xw[32 * w] = 0u;
+  long long best_f = LLONG_MAX;
+  int best_k = -1, nfeas = 0;
+  uint32_t c_flips = 0, c_unif = 0, c_fp64 = 0, c_unc = 0, c_philox = 0;
+  const uint2 key = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+  const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
+  const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
+  const int Wn = (n + 31) >> 5;
+  uint32_t pf = 0;                                     // groups taken from the producer so far
+  int loff = 0;                                        // buffer of the current group (0 without producers)
+
+  for (int k = 0; k < a.K; ++k) {
+    // ---- per-iteration constants: c_l Lambda_m (rounded once), error-bound slope E1 ----
+    float cLmax = 0.0f;
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      cL[m] = (float)(c_l * (double)Lam[32 * m]);
+      cLmax = fmaxf(cLmax, fabsf(cL[m]));
+    }
+    // |z_f32 - z| <= beta (E1 |A_i|_1 + E0_i) + 2^-23 |z|, E = (MM+8) 2^-24 (...):
+    // the lookahead's band value adds |A_i . A_{i-1}| <= |A_i|_1 max A; factor 2: safety margin.
+    // + 2^-22 |z| folded in with |z| <= beta (|c_o c_i| + c_p a_i + |A_i|_1 (2 c_p r_max + max|c_l Lambda|))
+    const double Wk = 2.0 * c_p * ((double)rbound + (double)amax) + (double)cLmax;
+    const float E1 = (float)((MM + 8) * 0x1p-24 * Wk * 2.0 + 0x1p-22 * Wk * 1.01);
+
+    for (int t = 0; t < a.T; ++t) {
+      const bool bz = (a.T >= 2) && (t == 0);          // beta_0 = 0: x_i = [u < 1/2]
+      const double beta = (a.T >= 2) ? bstep * (double)t : a.beta_max;
+      const float bf = (float)beta;
+      uint32_t xcur = 0;
+
+      // Logits of the uniforms of spins 128g .. 128g+127 (R2: the Philox call of counter
+      // (32g + j, t, k, s<<20|rho) yields the words of spins 128g + 32w + j, w = 0..3).  They do
+      // not depend on the state, so they are drawn in one ILP-friendly burst per group, off the
+      // sequential dependency chain of the decisions.
+      auto fill_words = [&](int g, auto NW) {              // NW = words of the group holding spins
+#pragma unroll 4
+        for (int j = 0; j < 32; ++j) {
+          const uint4 w4 = philox_group(key, g, j, t, k, srho);
+          lt[32 * (j + 0)] = logit_signed(w4.x);
+          if (NW.value > 1) lt[32 * (j + 32)] = logit_signed(w4.y);
+          if (NW.value > 2) lt[32 * (j + 64)] = logit_signed(w4.z);
+          if (NW.value > 3) lt[32 * (j + 96)] = logit_signed(w4.w);
+        }
+      };
+      auto fill_group = [&](int g) {
+        if (prod) {                                        // the producer's buffer (g & 1)
+          if (pf >= 1) mbar_arrive(mb + 2 + ((pf - 1u) & 1u));   // done with the previous group
+          mbar_wait(mb + (pf & 1u), (pf >> 1) & 1u);
+          loff = (int)(pf & 1u) * (32 * 128);
+          ++pf;
+        } else {
+          const int nw = min(4, (N - 128 * g + 31) >> 5);
+          if (nw >= 4) fill_words(g, std::integral_constant<int, 4>{});
+          else if (nw == 3) fill_words(g, std::integral_constant<int, 3>{});
+          else if (nw == 2) fill_words(g, std::integral_constant<int, 2>{});
+          else fill_words(g, std::integral_constant<int, 1>{});
+        }
+        c_philox += 32;
+      };
+      // Certified decision [u < sigma(z)] (R18, R19) from z, its error bound e and l = logit(u)
+      // (exact sign), evaluated branch-free; only the rare fp64 re-evaluation (slow(): returns
+      // x | uncertified << 1) sits behind a warp vote.
+      auto decide = [&](float z, float e, float l, auto slow) -> int {
+        // e bounds |z_f32 - z| for every reachable state and does not depend on z, so both
+        // thresholds are ready before z: the dependency chain is z -> d -> compare.
+        const float satT = e + kSatThr;
+        const float certT = (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f;
+        const float d = z - l;
+        const bool sat = fabsf(z) > satT;
+        int nx = sat ? (z > 0.0f) : (d > 0.0f);
+        if (bz) nx = (int)(__float_as_uint(l) >> 31);     // beta_0 = 0: u < 1/2 (sign bit, -0 included)
+        c_unif += (!bz && !sat) ? 1u : 0u;
+        const bool need = !bz && !sat && !(fabsf(d) > certT);
+        if (__any_sync(kFull, need)) {
+          if (need) {
+            ++c_fp64;
+            const int rs = slow();
+            if (rs & 2) ++c_unc;
+            nx = rs & 1;
+          }
+        }
+        return nx;
+      };
+
+      // ---- items i = 0..n-1, with a one-spin lookahead ----
+      // pre = A_i . r evaluated with r as it was BEFORE the decision of spin i-1 (so it is computed
+      // off the sequential dependency chain, during step i-1); the exact dot follows from one fma
+      // with the band value G_i = A_i . A_{i-1}:  A_i . r_now = pre + delta_{i-1} G_i.
+      auto dots = [&](int i, float &pr, float &dlv) {
+        const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
+        // four partial sums per dot product (short dependency chains; each term still passes at
+        // most MA/4 + 2 roundings, inside the (MM + 8) 2^-24 bound of E1)
+        float dr0 = 0.f, dr1 = 0.f, dr2 = 0.f, dr3 = 0.f, dl0 = 0.f, dl1 = 0.f, dl2 = 0.f, dl3 = 0.f;
+#pragma unroll
+        for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
+          const float4 av = Ac[m4];
+          dr0 = fmaf(av.x, r[4 * m4 + 0], dr0);
+          dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0);
+          if (4 * m4 + 1 < MA) { dr1 = fmaf(av.y, r[4 * m4 + 1], dr1); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1); }
+          if (4 * m4 + 2 < MA) { dr2 = fmaf(av.z, r[4 * m4 + 2], dr2); dl2 = fmaf(av.z, cL[4 * m4 + 2], dl2); }
+          if (4 * m4 + 3 < MA) { dr3 = fmaf(av.w, r[4 * m4 + 3], dr3); dl3 = fmaf(av.w, cL[4 * m4 + 3], dl3); }
+        }
+        pr = (dr0 + dr1) + (dr2 + dr3);
+        dlv = (dl0 + dl1) + (dl2 + dl3);
+      };
+      float pre = 0.f, dlc = 0.f, dprev = 0.f, Gc = 0.f;
+      dots(0, pre, dlc);                                  // (column n is zero: the lookahead past n-1 is harmless)
+      for (int w = 0; 32 * w < n; ++w) {
+        xcur = xw[32 * w];
+        if ((w & 3) == 0) fill_group(w >> 2);
+        const int iend = min(32, n - 32 * w);
+        // state-independent operands of the current step, prefetched one step ahead
+        float l = lt[loff + 32 * ((32 * w) & 127)];
+        float4 ic = sIc[32 * w];                          // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
+        float G_n = sBand[32 * w + 1];
+        for (int ii = 0; ii < iend; ++ii) {
+          const int i = 32 * w + ii;
+          const float l_n = lt[loff + 32 * ((i + 1) & 127)];     // valid for ii + 1 < iend (same group)
+          const float4 ic_n = sIc[i + 1];                 // padded entry n
+          const float G_nn = sBand[i + 2 <= n ? i + 2 : n];
+          const int xb = (xcur >> ii) & 1u;
+          const float dr = fmaf(dprev, Gc, pre);          // A_i . r (current state)
+          float pre_n, dl_n;
+          dots(i + 1, pre_n, dl_n);                       // lookahead (independent of this decision)
+          const float sg = xb ? -1.0f : 1.0f;             // 1 - 2 x_i
+          const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
+          const float z = bf * F;
+          const float e = bf * fmaf(E1, ic.z, ic.w);
+          const int nx = decide(z, e, l, [&]() -> int {
+            const uint32_t wd = word_of(key, i, t, k, srho);
+            double drd = 0.0, dld = 0.0, a2 = 0.0;
+#pragma unroll
+            for (int m = 0; m < MM; ++m) {
+              const double Am = (double)sAcol[i * MM + m];
+              drd += Am * (double)r[m];
+              dld += Am * (double)Lam[32 * m];
+              a2 += Am * Am;
+            }
+            const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * drd, t4 = c_l * dld;
+            const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
+            const int rs = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), wd);
+            if constexpr (RP) {                          // double-double level: replay kernel only
+              if ((rs & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
+                // double-double level on the exact integers (drd, a2 exact in fp64; kappa in int64)
+                long long kap = 0;
+                for (int m = 0; m < MA; ++m) kap += (long long)sAcol[i * MM + m] * Lam[32 * m];
+                return decide_dd(-(long long)sC[i], 2 * (long long)drd + (long long)a2 * (1 - 2 * xb), kap, a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, wd);
+              }
+            }
+            return rs;
+          });
+          const float dl = (float)(nx - xb);              // delta in {-1, 0, +1}; fma(0, A, r) == r
+          const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
+#pragma unroll
+          for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
+            const float4 av = Ac[m4];
+            r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
+            if (4 * m4 + 1 < MA) r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
+            if (4 * m4 + 2 < MA) r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
+            if (4 * m4 + 3 < MA) r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
+          }
+          xcur ^= (uint32_t)(nx != xb) << ii;
+          c_flips += (nx != xb) ? 1u : 0u;
+          pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
+          l = l_n; ic = ic_n; G_n = G_nn;
+        }
+        xw[32 * w] = xcur;
+      }
+      // ---- slack bits: row m, bit q, spin i = n + sum_{m'<m} q_m' + q (R4) ----
+      int i = n;
+      xcur = xw[32 * (n >> 5)];                            // word holding spin n (stored by the item loop)
+#pragma unroll
+      for (int m = 0; m < MA; ++m) {
+        const int qm = (m < M) ? sQ[m] : 0;
+        for (int q = 0; q < qm; ++q, ++i) {
+          if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
+          if ((i & 127) == 0) fill_group(i >> 7);
+          const float l = lt[loff + 32 * (i & 127)];
+          const int xb = (xcur >> (i & 31)) & 1u;
+          const float A = (float)(1u << q);
+          const float sg = xb ? -1.0f : 1.0f;
+          const float inner = fmaf(twocp, r[m], cL[m]);
+          const float F = -(A * inner) - (cpf * A) * A * sg;
+          const float z = bf * F;
+          // |z_f32 - z| <= beta (8 2^-24 + 1.01 2^-22) (A (|2 c_p r_m| + |c_l Lambda_m|) + c_p A^2)
+          const float e = bf * (8.0f * 0x1p-24f + 1.01f * 0x1p-22f) *
+                          fmaf(A, fabsf(twocp * r[m]) + fabsf(cL[m]), cpf * A * A);
+          const int nx = decide(z, e, l, [&]() -> int {
+            const uint32_t w = word_of(key, i, t, k, srho);
+            const double Ad = (double)A;
+            const double t1 = Ad * 2.0 * c_p * (double)r[m], t2 = Ad * c_l * (double)Lam[32 * m];
+            const double t3 = c_p * Ad * Ad;
+            const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
+            const int rs = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
+            if constexpr (RP) {                          // double-double level: replay kernel only
+              if ((rs & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
+                const long long Ai = 1LL << q;
+                return decide_dd(0, 2 * Ai * (long long)r[m] + Ai * Ai * (1 - 2 * xb), Ai * Lam[32 * m], a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, w);
+              }
+            }
+            return rs;
+          });
+          r[m] = fmaf((float)(nx - xb), A, r[m]);
+          xcur ^= (uint32_t)(nx != xb) << (i & 31);
+          c_flips += (nx != xb) ? 1u : 0u;
+          if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
+        }
+      }
+    }
+
+    // ---- readout of x_k: f, feasibility, trace, best, Lagrange step ----
+    long long f = 0;
+    for (int w = 0; w < Wn; ++w) {
+      uint32_t bits = xw[32 * w];
+      if (32 * w + 32 > n) bits &= (1u << (n - 32 * w)) - 1u;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        f += sC[32 * w + b];
+      }
+    }
+    // feasible <=> A x_items <= b  <=>  r_m <= (slack value of row m) for every row (R12)
+    bool feas = true;
+    {
+      int i0 = n;
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const int qm = (m < M) ? sQ[m] : 0;
+        if (qm > 0) {
+          long long sv = 0;
+          for (int q = 0; q < qm; ++q) {
+            const int i = i0 + q;
+            sv += (long long)((xw[32 * (i >> 5)] >> (i & 31)) & 1u) << q;
+          }
+          if ((long long)r[m] > sv) feas = false;
+        }
+        i0 += qm;
+      }
+    }
+    const size_t row = ((size_t)s * a.R + ridx) * a.K + k;
+    if (live) {
+      if (a.out.tr_f) a.out.tr_f[row] = f;
+      if (a.out.tr_feas) a.out.tr_feas[row] = (uint8_t)feas;
+      for (int m = 0; m < M; ++m) {
+        if (a.out.tr_lam) a.out.tr_lam[row * M + m] = Lam[32 * m];
+      }
+      if (a.out.tr_x)
+        for (int w = 0; w < a.WN; ++w) a.out.tr_x[row * a.WN + w] = xw[32 * w];
+    }
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      if (m < M) {
+        const long long rl = (long long)r[m];
+        if (live && a.out.tr_r) a.out.tr_r[row * M + m] = rl;
+        Lam[32 * m] += rl;                                 // lambda_{k+1} = lambda_k + eta g(x_k) (R10)
+      }
+    }
+    if (feas) {
+      ++nfeas;
+      if (f < best_f) {
+        best_f = f;
+        best_k = k;
+        if (live) {
+          const size_t ri = (size_t)s * a.R + ridx;
+          for (int w = 0; w < Wn; ++w) {
+            uint32_t bits = xw[32 * w];
+            if (32 * w + 32 > n) bits &= (1u << (n - 32 * w)) - 1u;
+            a.out.best_x[ri * a.Wn + w] = bits;
+          }
+        }
+      }
+    }
+  }
+
+  // ---- outputs ----
+  const size_t ri = (size_t)s * a.R + ridx;
+  if (live) {
+    a.out.best_f[ri] = best_f;
+    a.out.best_k[ri] = best_k;
+    a.out.n_feasible[ri] = nfeas;
+    if (best_k < 0)
+      for (int w = 0; w < Wn; ++w) a.out.best_x[ri * a.Wn + w] = 0u;
+    if (a.out.final_x)
+      for (int w = 0; w < a.WN; ++w) a.out.final_x[ri * a.WN + w] = xw[32 * w];
+    if (a.out.final_lam)
+      for (int m = 0; m < M; ++m) a.out.final_lam[ri * M + m] = Lam[32 * m];
+    if (a.out.rep_flips) a.out.rep_flips[ri] = c_flips;
+  }
+  // per-instance best (f << 20 | rho): warp min, one atomic
+  // Exact replay: the main kernel defers a warp in which some decision was not
+  // certified by the fp64 level (SAIM_FLAG_TEST_REPLAY: any fp64-level decision) -- the replay
+  // kernel re-runs its CTA with the double-double level and only the flagged warps contribute
+  // their instance-best candidates and counters (the others did in the main kernel).
+  const size_t rslot = replay_slot(cw);
+  const bool defer = !RP && __any_sync(kFull, live && (c_unc != 0 || ((a.flags & SAIM_FLAG_TEST_REPLAY) && c_fp64 != 0)));
+  const bool contribute = RP ? a.replay[rslot] != 0 : !defer;
+  if (defer) {
+    const uint32_t nrep = __popc(__ballot_sync(kFull, live));
+    if (lane == 0) {
+      a.replay[rslot] = 1;
+      if (a.out.counters) atomicAdd(reinterpret_cast<unsigned long long *>(a.out.counters) + SAIM_CNT_REPLAYED, (unsigned long long)nrep);
+    }
+  }
+  long long key_best = (live && best_k >= 0) ? ((best_f << 20) | (long long)rho) : LLONG_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long other = __shfl_xor_sync(kFull, key_best, o);
+    key_best = other < key_best ? other : key_best;
+  }
+  if (contribute && lane == 0 && key_best != LLONG_MAX && a.out.inst_best)
+    atomicMin(reinterpret_cast<long long *>(a.out.inst_best) + s, key_best);
+  if (a.out.counters && contribute) {
+    const unsigned long long nl = live ? 1ull : 0ull;
+    const unsigned long long fl = warp_sum_u64(nl * c_flips), un = warp_sum_u64(nl * c_unif);
+    const unsigned long long fp = warp_sum_u64(nl * c_fp64), uc = warp_sum_u64(nl * c_unc);
+    const unsigned long long ph = warp_sum_u64(nl * c_philox), nf = warp_sum_u64(nl * (unsigned long long)nfeas);
+    const unsigned long long lv = warp_sum_u64(nl);
+    if (lane == 0) {
+      unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
+      atomicAdd(c + SAIM_CNT_DECISIONS, lv * (unsigned long long)a.K * a.T * N);
+      atomicAdd(c + SAIM_CNT_FLIPS, fl);
+      atomicAdd(c + SAIM_CNT_SWEEPS, lv * (unsigned long long)a.K * a.T);
+      atomicAdd(c + SAIM_CNT_UNIFORMS, un);
+      atomicAdd(c + SAIM_CNT_FP64, fp);
+      atomicAdd(c + SAIM_CNT_UNCERTIFIED, uc);
+      atomicAdd(c + SAIM_CNT_FEASIBLE, nf);
+      atomicAdd(c + SAIM_CNT_PHILOX, ph);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+typedef void (*mkp_kernel_t)(const RunArgs);
+// (MM, M) -> kernel (RPV: the exact-replay instantiation).
+// Producer-warp instantiations exist for M <= 8 (where one consumer warp per SMSP is the norm).
+template <bool RPV>
+static mkp_kernel_t mkp_kernel_for_t(int MM, int M, bool prod) {
+  if (prod) {
+    if (MM == 8 && M == 5) return saim_mkp_kernel<8, 5, true, RPV>;
+    if (MM == 4) return saim_mkp_kernel<4, 4, true, RPV>;
+    if (MM == 8) return saim_mkp_kernel<8, 8, true, RPV>;
+    return nullptr;
+  }
+  if (MM == 8 && M == 5) return saim_mkp_kernel<8, 5, false, RPV>;
+  if (MM == 16 && M == 10) return saim_mkp_kernel<16, 10, false, RPV>;
+  if (MM == 32 && M == 30) return saim_mkp_kernel<32, 30, false, RPV>;
+  switch (MM) {
+    case 4: return saim_mkp_kernel<4, 4, false, RPV>;
+    case 8: return saim_mkp_kernel<8, 8, false, RPV>;
+    case 16: return saim_mkp_kernel<16, 16, false, RPV>;
+    case 32: return saim_mkp_kernel<32, 32, false, RPV>;
+    default: return nullptr;
+  }
+}
+
+
+}  // namespace saim

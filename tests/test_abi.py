@@ -69,7 +69,7 @@ def test_create_rejects_bad_input_without_gpu():
     with pytest.raises(P.SaimError) as ei:
         P.Solver(big, [[0, 0], [0, 0]], [[[1, 1], [1, 1]], [[1, 1], [1, 1]]], [[1, 1], [1, 1]], 1.0, 1.0, 1.0)
     assert ei.value.code == P.SAIM_EUNSUPPORTED                             # quadratic with M = 2
-    for bad in (128, P.FLAG_MKP_LOCKSTEP | P.FLAG_MKP_L2, P.FLAG_MKP_L2 | P.FLAG_MKP_L4, P.FLAG_MKP_SPLIT2 | P.FLAG_MKP_L4):
+    for bad in (256, P.FLAG_MKP_LOCKSTEP | P.FLAG_MKP_L2, P.FLAG_MKP_L2 | P.FLAG_MKP_L4, P.FLAG_MKP_SPLIT2 | P.FLAG_MKP_L4):
         with pytest.raises(P.SaimError) as ei:                              # unknown / conflicting flags
             P.Solver(None, [0, 0], [[1, 1], [1, 0]], [3, 1], 1.0, 1.0, 1.0, flags=bad)
         assert ei.value.code == P.SAIM_EINVAL
@@ -77,9 +77,9 @@ def test_create_rejects_bad_input_without_gpu():
 
 def test_qkp_div_magic_table_is_exact():
     """The QKP hot step divides lane indices by the unsaturated width pw with the table
-    kDivMagic[p] = ceil(2^16 / p) (saim_qkp.cu): (x * m) >> 16 == x // p for every x <= 32."""
+    kDivMagic[p] = ceil(2^16 / p) (saim_qkp.cuh): (x * m) >> 16 == x // p for every x <= 32."""
     import re
-    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2501_04971_b200", "csrc", "saim_qkp.cu")).read()
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2501_04971_b200", "csrc", "saim_qkp.cuh")).read()
     body = re.search(r"kDivMagic\[33\]\s*=\s*\{([^}]*)\}", src).group(1)
     mag = [int(v) for v in body.replace("\n", " ").split(",") if v.strip()]
     assert len(mag) == 33

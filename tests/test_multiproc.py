@@ -1,6 +1,9 @@
-"""The N > 1 path on CPU: world_size-2 gloo processes shard the replicas by global index, run their
-shard (through the oracle -- the CUDA kernels need a GPU), and all-reduce(MIN) the packed
-per-instance best.  The result must equal one process running every replica."""
+"""The N > 1 path on CPU: world_size-2 gloo processes shard the replicas by global index, compute
+their shard (through the oracle -- the CUDA kernels need a GPU -- written into the same output dict
+saim_run fills: inst_best keys and per-replica best_x), and run the end-of-run exchange with the
+function bench.py calls (dist.finalize: all-reduce(MIN) of the packed per-instance best, then the
+winning replica's bitset from its owner).  The result must equal one process running every replica
+(DESIGN.md section 8)."""
 import os
 import socket
 
@@ -31,12 +34,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_path):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _shard_outputs(rep0, R):
+    """What saim_run returns for replicas [rep0, rep0 + R) of every instance (inst_best = min packed
+    key over the shard, best_x per replica), computed by the oracle."""
     probs, Ps, eta, bmax = _instances()
-    rep0, R = sdist.shard_range(rank, world, R_PER_RANK)
-    keys = []
+    keys, bx = [], []
     for s, prob in enumerate(probs):
         op = oracle.OracleProblem.from_inputs(prob, Ps[s], eta, bmax, inst=s)
         res = op.run(SEED, R, K, T, rep0=rep0, nthreads=2)
@@ -45,28 +47,44 @@ def _worker(rank, world, port, out_path):
             if res["best_k"][j] >= 0:
                 best = min(best, sdist.pack_best(res["best_f"][j], rep0 + j))
         keys.append(best)
-    t = torch.tensor(keys, dtype=torch.int64)
-    sdist.reduce_inst_best(t)
-    if rank == 0:
-        np.save(out_path, t.numpy())
+        bx.append(res["best_x"].view(np.int32))
+    return {"inst_best": torch.tensor(keys, dtype=torch.int64), "best_x": torch.from_numpy(np.stack(bx))}
+
+
+def _worker(rank, world, port, out_path, reverse):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # reverse: rank r owns the range of rank world-1-r, so the winners (lowest replica index on
+    # ties) live on the last rank and the bitset must travel to rank 0
+    rep0, R = sdist.shard_range(world - 1 - rank if reverse else rank, world, R_PER_RANK)
+    out = _shard_outputs(rep0, R)
+    win_x = sdist.finalize(out, rep0, R)          # the exchange bench.py runs after every step
+    np.save(out_path + f".{rank}.npy", np.concatenate([out["inst_best"].numpy(), win_x.numpy().ravel()]))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_two_rank_sharding_equals_single_run(tmp_path):
-    out = str(tmp_path / "keys.npy")
-    mp.start_processes(_worker, args=(2, _free_port(), out), nprocs=2, join=True, start_method="spawn")
-    got = np.load(out)
+@pytest.mark.parametrize("reverse", [False, True])
+def test_two_rank_sharding_equals_single_run(tmp_path, reverse):
+    out = str(tmp_path / "keys")
+    mp.start_processes(_worker, args=(2, _free_port(), out, reverse), nprocs=2, join=True, start_method="spawn")
+    ranks = [np.load(out + f".{r}.npy") for r in range(2)]
+    assert np.array_equal(ranks[0], ranks[1])          # every rank holds the same result
     probs, Ps, eta, bmax = _instances()
+    S = len(probs)
+    got_keys, got_x = ranks[0][:S], ranks[0][S:].reshape(S, -1)
     for s, prob in enumerate(probs):
         op = oracle.OracleProblem.from_inputs(prob, Ps[s], eta, bmax, inst=s)
         res = op.run(SEED, 2 * R_PER_RANK, K, T, nthreads=4)
-        want = sdist.I64_MAX
+        want, wj = sdist.I64_MAX, None
         for j in range(2 * R_PER_RANK):
-            if res["best_k"][j] >= 0:
-                want = min(want, sdist.pack_best(res["best_f"][j], j))
-        assert int(got[s]) == want
-    assert all(int(k) != sdist.I64_MAX for k in got)   # both instances reach feasible samples
+            if res["best_k"][j] >= 0 and sdist.pack_best(res["best_f"][j], j) < want:
+                want, wj = sdist.pack_best(res["best_f"][j], j), j
+        assert int(got_keys[s]) == want
+        assert np.array_equal(got_x[s].astype(np.int32).view(np.uint32), res["best_x"][wj])
+        f, rho = sdist.unpack_best(int(got_keys[s]))
+        assert rho == wj and f == res["best_f"][wj]
+    assert all(int(k) != sdist.I64_MAX for k in got_keys)   # both instances reach feasible samples
 
 
 def test_shard_range_and_packing():
