@@ -3,11 +3,10 @@
 
 #ifdef SAIM_PROF
 // Development profiling build only (-DSAIM_PROF): per-sweep clock64 totals by phase of the anneal.
-__device__ unsigned long long saim_prof[8];
 extern "C" int saim_prof_read(unsigned long long *h, int reset) {
   cudaMemcpyFromSymbol(h, saim_prof, sizeof(saim_prof));
   if (reset) {
-    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long z[48] = {0};
     cudaMemcpyToSymbol(saim_prof, z, sizeof(z));
   }
   return 0;

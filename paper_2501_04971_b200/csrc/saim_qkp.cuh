@@ -30,7 +30,7 @@
 #include "saim_dev.cuh"
 
 #ifdef SAIM_PROF
-extern __device__ unsigned long long saim_prof[8];   // saim_qkp.cu (profiling build only)
+__device__ unsigned long long saim_prof[48];  // profiling build only (read by saim_prof_read, saim_qkp.cu)
 #endif
 
 namespace saim {
@@ -75,7 +75,7 @@ struct WarpState {
   uint32_t srho;                    // (s << 20) | rho
   uint32_t uw[4][32];               // lazily drawn words of the current group, per lane
 #ifdef SAIM_PROF
-  unsigned long long prof[8];
+  uint32_t prof[48];               // per 1/16 of the anneal: cycles, sweep-loop iterations, flips
 #endif
 };
 enum { kCntFlips = 0, kCntUnif, kCntFp64, kCntUncert, kCntPhilox, kCntSweeps };
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     ws->best_k = -1;
     ws->nfeas = 0;
 #ifdef SAIM_PROF
-    for (int i = 0; i < 8; ++i) ws->prof[i] = 0;
+    for (int i = 0; i < 48; ++i) ws->prof[i] = 0;
 #endif
 #pragma unroll
     for (int i = 0; i < 6; ++i) ws->cnt[i] = 0;
@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     for (int t = t0; t < a.T; ++t) {
 #ifdef SAIM_PROF
       const long long prof_c0 = clock64();
+      const uint32_t prof_f0 = nflip;
 #endif
       // ---- Hot-block loop ----
       // Every block but one (b) is certified quiet: those keep their spins whatever happens in b
@@ -695,9 +696,10 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       // grows, so every later sweep of this anneal is certified the same way -- x_k is final.
 #ifdef SAIM_PROF
       if (lane == 0) {
-        const int pb = t < a.T / 10 ? 0 : (t < (3 * a.T) / 10 ? 1 : 2);
-        ws->prof[pb] += (unsigned long long)(clock64() - prof_c0);
-        ws->prof[4 + pb] += 1ull;
+        const int pb = min(15, (int)(16LL * t / a.T));
+        ws->prof[pb] += (uint32_t)(clock64() - prof_c0);
+        ws->prof[16 + pb] += 1u;
+        ws->prof[32 + pb] += nflip - prof_f0;
       }
 #endif
       if (!active && freeze_exit && a.T >= 2) {
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   }
 #ifdef SAIM_PROF
   if (lane == 0)
-    for (int i = 0; i < 8; ++i) atomicAdd(&saim_prof[i], ws->prof[i]);
+    for (int i = 0; i < 48; ++i) atomicAdd(&saim_prof[i], (unsigned long long)ws->prof[i]);
 #endif
   if (lane == 0 && a.out.counters && !defer) {
     unsigned long long *c = reinterpret_cast<unsigned long long *>(a.out.counters);
