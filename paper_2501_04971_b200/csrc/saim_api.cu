@@ -16,7 +16,10 @@
 #include <string>
 #include <vector>
 
+#include <mutex>
+
 #include "../../include/saim.h"
+#include "saim_dev.cuh"
 #include "saim_layout.h"
 
 namespace saim {
@@ -38,6 +41,35 @@ int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double
 using namespace saim;
 
 static thread_local std::string g_err;
+
+// The fp64 slow path's logit table (saim_dev.cuh logit_f64): one per device, built on first use
+// and kept for the life of the process (64 MB).
+__global__ void saim_logit_table_kernel(double *t) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < (1u << 23)) t[m] = logit_f64_calc(m << 9);
+}
+
+static std::mutex g_tab_mu;
+static double *g_tab[64] = {};
+
+static cudaError_t logit_table(int dev, const double **out) {
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!g_tab[dev]) {
+    double *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sizeof(double) << 23);
+    if (e != cudaSuccess) return e;
+    saim_logit_table_kernel<<<(1u << 23) / 256, 256>>>(p);
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      return e;
+    }
+    g_tab[dev] = p;
+  }
+  *out = g_tab[dev];
+  return cudaSuccess;
+}
 
 static int fail(int code, const char *fmt, ...) {
   char buf[512];
@@ -219,6 +251,11 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
 
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "cudaSetDevice"); }
+  {
+    const double *tab = nullptr;
+    if ((e = logit_table(ctx->device, &tab)) != cudaSuccess) { delete ctx; return cuda_fail(e, "logit table"); }
+    for (int s = 0; s < S; ++s) ctx->hdr[s].logit_tab = tab;
+  }
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device);

@@ -42,6 +42,7 @@ struct InstHdr {
   double v_bound;     // 2 max|r| + max A_ext      >= |2 r0 + A_i| for every state
   double r_bound;     // max|r_k| over every state and row (host-proven)
   double P, eta, beta_max;  // the run constants exactly as given (double-double slow path, R18)
+  const double *logit_tab;  // logit((2m+1) 2^-24) for m < 2^23 (fp64 slow path; one table per device)
 };
 
 inline __host__ __device__ uint32_t align16u(uint32_t v) { return (v + 15u) & ~15u; }

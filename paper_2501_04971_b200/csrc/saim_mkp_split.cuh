@@ -29,7 +29,7 @@ constexpr uint32_t kFull = 0xffffffffu;
 constexpr int kSplitThreads = 512;
 
 __device__ __forceinline__ int certify_fp64_s(double zz, double S, uint32_t w) {
-  const double d = zz - logit_f64(w);
+  const double d = zz - logit_f64_calc(w);
   return (d > 0.0 ? 1 : 0) | (fabs(d) <= (S + 1.0 + fabs(zz)) * 0x1p-46 ? 2 : 0);
 }
 

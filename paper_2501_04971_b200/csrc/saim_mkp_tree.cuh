@@ -46,7 +46,7 @@ __device__ __noinline__ uint32_t word_of_t(uint2 key, int i, int t, int k, uint3
 // fp64 tail of the slow path: z and its magnitude sum S are accurate to ~2^-50 S; returns
 // (x | uncertified << 1).
 __device__ __noinline__ int certify_fp64_t(double zz, double S, uint32_t w) {
-  const double d = zz - logit_f64(w);
+  const double d = zz - logit_f64_calc(w);
   return (d > 0.0 ? 1 : 0) | (fabs(d) <= (S + 1.0 + fabs(zz)) * 0x1p-46 ? 2 : 0);
 }
 

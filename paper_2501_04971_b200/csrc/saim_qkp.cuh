@@ -99,7 +99,7 @@ __device__ __noinline__ int decide_fp64(float phib, float v, float A, int t, con
   const double Ad = (double)A, vd = (double)v, pd = (double)phib;
   const double z = fma(K1d, pd, -(Ad * fma(K2d, vd, K3d)));
   const double S = fabs(K1d * pd) + fabs(Ad) * (fabs(K2d * vd) + fabs(K3d));
-  const double d = z - logit_f64(w);
+  const double d = z - logit_f64(H, w);
   const double e = (S + 1.0 + fabs(z)) * 0x1p-47;
   if constexpr (!RP) {
     return (d > 0.0 ? 1 : 0) | (fabs(d) <= e ? 2 : 0);
