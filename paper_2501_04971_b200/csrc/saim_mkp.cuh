@@ -337,13 +337,19 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // ---- slack bits: row m, bit q, spin i = n + sum_{m'<m} q_m' + q (R4) ----
       int i = n;
       xcur = xw[32 * (n >> 5)];                            // word holding spin n (stored by the item loop)
+      // logit of the current slack spin, loaded one step ahead (the loads are off the decision
+      // chain; at a group boundary the new group is filled first and the logit reloaded)
+      float l = lt[loff + 32 * (n & 127)];
 #pragma unroll
       for (int m = 0; m < MA; ++m) {
         const int qm = (m < M) ? sQ[m] : 0;
         for (int q = 0; q < qm; ++q, ++i) {
           if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
-          if ((i & 127) == 0) fill_group(i >> 7);
-          const float l = lt[loff + 32 * (i & 127)];
+          if ((i & 127) == 0) {
+            fill_group(i >> 7);
+            l = lt[loff];
+          }
+          const float l_n = lt[loff + 32 * ((i + 1) & 127)];   // valid unless i + 1 starts a group
           const int xb = (xcur >> (i & 31)) & 1u;
           const float A = (float)(1u << q);
           const float sg = xb ? -1.0f : 1.0f;
@@ -372,6 +378,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
           xcur ^= (uint32_t)(nx != xb) << (i & 31);
           c_flips += (nx != xb) ? 1u : 0u;
           if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
+          l = l_n;
         }
       }
     }
