@@ -174,7 +174,10 @@ void saim_destroy(saim_ctx *ctx);
  *  which = 2: the double-double decision level (R18) on n records; in_u32 points to n
  *             80-byte records {int64 phi, pi, kappa, s_o, s_c; double P, eta, beta_max; int32 tn,
  *             td; uint32 w; int32 pad} (beta_t = beta_max tn/td, u from the Philox word w as in R2);
- *             out_u32[i] = x | (uncertified << 1) for record i. */
+ *             out_u32[i] = x | (uncertified << 1) for record i.
+ *  which = 3: the fp64 slow path's logit table (one per device, built by saim_create): for n Philox
+ *             words in_u32, out_f64[2i] = the table entry the slow path reads, out_f64[2i+1] =
+ *             ln(u) - ln(1 - u) computed directly on the device (must be identical). */
 int saim_selftest(int which, int device, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 
 /* Thread-local message of the last failing call ("" if none). */

@@ -242,6 +242,14 @@ def selftest_decide_dd(records, device: int = 0):
     return out
 
 
+def selftest_logit_table(words, device: int = 0):
+    """saim_selftest(3): (table entry, direct device computation) of logit(u) for each Philox word."""
+    w = np.ascontiguousarray(np.asarray(words, dtype=np.uint32).ravel())
+    out = np.zeros((w.shape[0], 2), np.float64)
+    _check(load_library().saim_selftest(3, int(device), w.shape[0], w.ctypes.data, None, out.ctypes.data))
+    return out[:, 0], out[:, 1]
+
+
 def selftest_logit(device: int = 0):
     out = np.zeros(2, np.float64)
     _check(load_library().saim_selftest(1, int(device), 0, None, None, out.ctypes.data))

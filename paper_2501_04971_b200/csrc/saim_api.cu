@@ -52,6 +52,18 @@ __global__ void saim_logit_table_kernel(double *t) {
 static std::mutex g_tab_mu;
 static double *g_tab[64] = {};
 
+// saim_selftest(3): the table's entries (through the slow path's accessor) next to a direct
+// computation, for given Philox words.
+__global__ void saim_selftest_logit_table_kernel(const double *tab, const uint32_t *w, double *out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  InstHdr h;
+  memset(&h, 0, sizeof(h));
+  h.logit_tab = tab;
+  out[2 * i] = logit_f64(&h, w[i]);
+  out[2 * i + 1] = logit_f64_calc(w[i]);
+}
+
 static cudaError_t logit_table(int dev, const double **out) {
   std::lock_guard<std::mutex> lk(g_tab_mu);
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
@@ -554,11 +566,25 @@ extern "C" void saim_destroy(saim_ctx *ctx) {
 
 extern "C" int saim_selftest(int which, int device, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64) {
   g_err.clear();
-  if (((which == 0 || which == 2) && (n < 1 || !in_u32 || !out_u32)) || (which == 1 && !out_f64) || which < 0 ||
-      which > 2)
+  if (((which == 0 || which == 2) && (n < 1 || !in_u32 || !out_u32)) || (which == 1 && !out_f64) ||
+      (which == 3 && (n < 1 || !in_u32 || !out_f64)) || which < 0 || which > 3)
     return fail(SAIM_EINVAL, "bad selftest arguments");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  if (which == 3) {
+    const double *tab = nullptr;
+    if ((e = logit_table(device, &tab)) != cudaSuccess) return cuda_fail(e, "logit table");
+    uint32_t *d_w = nullptr;
+    double *d_o = nullptr;
+    if ((e = cudaMalloc(&d_w, sizeof(uint32_t) * (size_t)n)) != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    if ((e = cudaMalloc(&d_o, sizeof(double) * 2 * (size_t)n)) != cudaSuccess) { cudaFree(d_w); return cuda_fail(e, "cudaMalloc"); }
+    cudaMemcpy(d_w, in_u32, sizeof(uint32_t) * (size_t)n, cudaMemcpyHostToDevice);
+    saim_selftest_logit_table_kernel<<<(n + 127) / 128, 128>>>(tab, d_w, d_o, n);
+    e = cudaMemcpy(out_f64, d_o, sizeof(double) * 2 * (size_t)n, cudaMemcpyDeviceToHost);
+    cudaFree(d_w);
+    cudaFree(d_o);
+    return e == cudaSuccess ? SAIM_OK : cuda_fail(e, "selftest 3");
+  }
   if (selftest(which, n, in_u32, out_u32, out_f64) != 0) return fail(SAIM_ECUDA, "selftest failed");
   return SAIM_OK;
 }

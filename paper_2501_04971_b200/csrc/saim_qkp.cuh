@@ -582,18 +582,37 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
           const bool mine = lane >= lo && lane < hi;
           const bool sat = fabsf(z) * kZScale - S > kSatThr20;
           int nx = z > 0.0f;
-          const uint32_t need = __ballot_sync(kFull, mine && !sat);
-          if (need) {
-            drew |= need;
-            if (mine && !sat) {
-              const float d = z - l;
-              if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
-                nx = d > 0.0f;
-              } else {
+          if constexpr (NPL <= 4) {
+            // small instances (<= 128 items, configs 0-1): branch-free decision, only the rare
+            // fp64 re-evaluation behind a vote (measured 1.7-4% faster there; at NPL = 10 the
+            // branchy form below is 1% faster)
+            const bool ns = mine && !sat;
+            drew |= __ballot_sync(kFull, ns);
+            const float d = z - l;
+            if (ns) nx = d > 0.0f;
+            const bool band = ns && !(fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f);
+            if (__any_sync(kFull, band)) {
+              if (band) {
                 const int rs = decide_fp64<RP>(phib, v, A, a.T >= 2 ? t : 1, Hp, ws, w);
                 nx = rs & 1;
                 atomicAdd(&ws->cnt[kCntFp64], 1u);
                 if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
+              }
+            }
+          } else {
+            const uint32_t need = __ballot_sync(kFull, mine && !sat);
+            if (need) {
+              drew |= need;
+              if (mine && !sat) {
+                const float d = z - l;
+                if (fabsf(d) > (S * (1.0f / kZScale) + el) * 1.0001f) {
+                  nx = d > 0.0f;
+                } else {
+                  const int rs = decide_fp64<RP>(phib, v, A, a.T >= 2 ? t : 1, Hp, ws, w);
+                  nx = rs & 1;
+                  atomicAdd(&ws->cnt[kCntFp64], 1u);
+                  if (rs & 2) atomicAdd(&ws->cnt[kCntUncert], 1u);
+                }
               }
             }
           }

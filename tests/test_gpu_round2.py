@@ -260,3 +260,18 @@ def test_mkp_dd_level_in_kernels(P):
             for k in _ALL_OUT:
                 assert np.array_equal(base[k], dd[k]), (v, k)
         run_both(P, [prob], [si.paper_P(prob, 5.0)], 0.05, 50.0, seed=4, R=64, K=6, T=200, flags=P.FLAG_TEST_REPLAY)
+
+
+def test_logit_table_matches_direct_computation(P):
+    """The fp64 slow path reads logit(u) from a per-device table of all 2^23 uniforms: every entry it
+    reads (word w -> entry w >> 9) equals the device's direct ln(u) - ln(1 - u) bit for bit, and the
+    host's within a few ulps (R2's u = (2 floor(w / 2^9) + 1) 2^-24)."""
+    rng = np.random.default_rng(5)
+    words = np.concatenate([np.array([0, 511, 512, 1023, 2 ** 31 - 1, 2 ** 31, 2 ** 32 - 512, 2 ** 32 - 1], np.uint64),
+                            rng.integers(0, 2 ** 32, size=20000, dtype=np.uint64)]).astype(np.uint32)
+    tab, calc = P.selftest_logit_table(words)
+    assert np.array_equal(tab.view(np.uint64), calc.view(np.uint64))
+    u = (2.0 * (words >> 9).astype(np.float64) + 1.0) * 2.0 ** -24
+    host = np.log(u) - np.log1p(-u)
+    assert np.all(np.abs(tab - host) <= 4 * np.spacing(np.abs(host)) + 1e-300)
+    assert tab[4] < 0 < tab[5]                           # u < 1/2 <=> w < 2^31
