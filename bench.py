@@ -377,7 +377,7 @@ def main():
                        "l2": "flushed between steps (256 MiB write outside the timed events)",
                        "parallelism": f"replicas sharded over {world} GPU(s), global replica index keyed RNG"},
             "samples_per_s": samples_per_s,
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 3 * args.steps,   # per step: init, main SAIM kernel, exact-replay kernel
             "roofline": {"bound": "alu" if bind != "smem" else "smem",
                          "achieved": achieved / (1e12 if bind != "smem" else 1e9),
                          "peak": rm["peak_per_s"] / (1e12 if bind != "smem" else 1e9),
