@@ -99,6 +99,15 @@ typedef struct {
  * uncertified there, so it is re-decided at the double-double level (MKP: at once; QKP: by the
  * exact replay of the whole replica).  Results are identical either way; only slower. */
 #define SAIM_FLAG_TEST_REPLAY 128
+/* MKP, M <= 8: the speculative sub-warp kernel with G = 2, 4, 8, 16 or 32 lanes per replica (each
+ * lane owns one spin of the replica's current block of G spins; the first flipping lane of a round
+ * is applied and the later lanes are re-evaluated: DESIGN.md 6.5).  Counts as a kernel-selection
+ * flag (at most one of these and the four above).  SAIM_ESMEM if M > 8.  Identical results. */
+#define SAIM_FLAG_MKP_SPEC2 1024
+#define SAIM_FLAG_MKP_SPEC4 256
+#define SAIM_FLAG_MKP_SPEC8 512
+#define SAIM_FLAG_MKP_SPEC16 2048
+#define SAIM_FLAG_MKP_SPEC32 4096
 
 /* Outputs of saim_run: CALLER-OWNED DEVICE pointers (e.g. torch CUDA tensors), written
  * asynchronously on the run's stream.  R = replicas per instance, Wn = ceil(n/32),

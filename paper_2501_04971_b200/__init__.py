@@ -26,6 +26,11 @@ FLAG_MKP_L4 = 8            # MKP: outcome tree with 4 lanes per replica
 FLAG_MKP_SPLIT2 = 16       # MKP: constraint rows of a replica split over 2 lanes (M > 8)
 FLAG_MKP_NO_PRODUCER = 64  # MKP lockstep: consumer warps draw their own logits (identical results)
 FLAG_QKP_NO_HOT_LOOP = 32  # QKP: disable the hot-block loop (identical results)
+FLAG_MKP_SPEC4 = 256       # MKP (M <= 8): speculative sub-warp kernel, 4 lanes per replica
+FLAG_MKP_SPEC8 = 512       # ... 8 lanes per replica
+FLAG_MKP_SPEC2 = 1024      # ... 2 lanes per replica
+FLAG_MKP_SPEC16 = 2048     # ... 16 lanes per replica
+FLAG_MKP_SPEC32 = 4096     # ... 32 lanes per replica (one replica per warp)
 FLAG_TEST_REPLAY = 128     # test hook: every fp64-level decision re-decided in double-double (identical results)
 EXPORTS = ["saim_create", "saim_run", "saim_get_info", "saim_get_instance", "saim_destroy",
            "saim_last_error", "saim_selftest"]

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsaim.so")
 SOURCES = ["saim_api.cu", "saim_qkp.cu", "saim_qkp_replay.cu", "saim_mkp.cu", "saim_mkp_replay.cu", "saim_mkp_tree.cu",
-           "saim_mkp_tree_replay.cu", "saim_mkp_split.cu", "saim_mkp_split_replay.cu"]
+           "saim_mkp_tree_replay.cu", "saim_mkp_split.cu", "saim_mkp_split_replay.cu", "saim_mkp_spec.cu", "saim_mkp_spec_replay.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

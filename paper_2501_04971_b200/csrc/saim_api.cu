@@ -35,6 +35,10 @@ cudaError_t mkpt_launch(const RunArgs &a, int n_inst, int MM, int L, int wpc, ui
                         bool replay);
 int mkps_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, uint32_t *per_warp, int *max_wpc);
 cudaError_t mkps_launch(const RunArgs &a, int n_inst, int MM, int wpc, uint32_t per_warp, cudaStream_t st, bool replay);
+int mkpx_plan(int M, int N_max, int smem_optin, int MM, uint32_t blob_bytes, int G, uint32_t *table_bytes,
+              uint32_t *per_warp, int *max_wpc, int *regs);
+cudaError_t mkpx_launch(const RunArgs &a, int n_inst, int MM, int G, int wpc, uint32_t per_warp, cudaStream_t st,
+                        bool replay);
 int selftest(int which, int n, const uint32_t *in_u32, uint32_t *out_u32, double *out_f64);
 }  // namespace saim
 
@@ -104,8 +108,11 @@ struct saim_ctx {
   int npl = 0, qb = 0, pk = 0;  // QKP (pk: phi packed as two int16 per word)
   int lanes = 32;       // lanes per replica (QKP: 32; MKP: 1 lockstep, L = 2 or 4 outcome tree)
   int mm = 0;           // MKP padded constraint count
-  int mkp_kind = 0;     // MKP kernel: 0 lockstep, 1 outcome tree, 2 row split
+  int mkp_kind = 0;     // MKP kernel: 0 lockstep, 1 outcome tree, 2 row split, 3 speculative sub-warp
   uint32_t per_warp = 0;
+  uint32_t spec_fixed = 0;     // MKP speculative kernel: shared bytes per CTA besides the warps' (blob + spin table + static)
+  int spec_regs = 0;           // ... registers per thread
+  int smem_sm = 0;             // shared memory per SM
   uint32_t per_warp_prod = 0;  // MKP lockstep with producer warps: per-consumer region, max consumers per CTA
   int max_wpc_prod = 0;
   int N_max = 0, n_slack_max = 0;
@@ -152,7 +159,8 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     return fail(SAIM_EINVAL, "missing c/A/b/P array");
   if (!std::isfinite(par->eta) || par->eta < 0) return fail(SAIM_EINVAL, "eta must be finite and >= 0");
   if (!std::isfinite(par->beta_max) || par->beta_max <= 0) return fail(SAIM_EINVAL, "beta_max must be finite and > 0");
-  const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2;
+  const int xmask = SAIM_FLAG_MKP_SPEC2 | SAIM_FLAG_MKP_SPEC4 | SAIM_FLAG_MKP_SPEC8 | SAIM_FLAG_MKP_SPEC16 | SAIM_FLAG_MKP_SPEC32;
+  const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2 | xmask;
   if ((par->flags & ~(SAIM_FLAG_NO_FREEZE_EXIT | SAIM_FLAG_QKP_NO_HOT_LOOP | SAIM_FLAG_MKP_NO_PRODUCER | SAIM_FLAG_TEST_REPLAY | kmask)) || __builtin_popcount(par->flags & kmask) > 1)
     return fail(SAIM_EINVAL, "unknown or conflicting flags 0x%x", par->flags);
 
@@ -271,6 +279,7 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device);
+  cudaDeviceGetAttribute(&ctx->smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
 
   std::vector<unsigned char> blob;
   if (M <= 1) {
@@ -350,10 +359,27 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     ctx->smem_bytes = (int)(L.bytes + ctx->per_warp);
     // Default (measured on B200): outcome tree with L = 2 for M <= 8, the
     // lockstep kernel for M > 8; the row split (M > 8) only on request.
+    const int xmask = SAIM_FLAG_MKP_SPEC2 | SAIM_FLAG_MKP_SPEC4 | SAIM_FLAG_MKP_SPEC8 | SAIM_FLAG_MKP_SPEC16 | SAIM_FLAG_MKP_SPEC32;
+    const bool spec = (ctx->flags & xmask) != 0;
     const bool tree = (ctx->flags & (SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) ||
-                      (!(ctx->flags & SAIM_FLAG_MKP_LOCKSTEP) && M <= 8);
-    const bool split = !tree && MM >= 16 && (ctx->flags & SAIM_FLAG_MKP_SPLIT2);
-    if (tree) {   // outcome-tree kernel (saim_mkp_tree.cu)
+                      (!spec && !(ctx->flags & SAIM_FLAG_MKP_LOCKSTEP) && M <= 8);
+    const bool split = !tree && !spec && MM >= 16 && (ctx->flags & SAIM_FLAG_MKP_SPLIT2);
+    if (spec) {   // speculative sub-warp kernel (saim_mkp_spec.cu)
+      const int G = (ctx->flags & SAIM_FLAG_MKP_SPEC2) ? 2 : (ctx->flags & SAIM_FLAG_MKP_SPEC4) ? 4
+                    : (ctx->flags & SAIM_FLAG_MKP_SPEC8) ? 8 : (ctx->flags & SAIM_FLAG_MKP_SPEC16) ? 16 : 32;
+      uint32_t tb = 0, pw = 0;
+      int wpc = 0;
+      if (mkpx_plan(M, ctx->N_max, smem_optin, MM, L.bytes, G, &tb, &pw, &wpc, &ctx->spec_regs) != 0) {
+        delete ctx;
+        return fail(SAIM_ESMEM, "MKP speculative kernel (G=%d) has no instantiation for M=%d or does not fit shared memory", G, M);
+      }
+      ctx->lanes = G;
+      ctx->mkp_kind = 3;
+      ctx->per_warp = pw;
+      ctx->max_wpc = wpc;
+      ctx->smem_bytes = (int)(L.bytes + tb + pw);
+      ctx->spec_fixed = L.bytes + tb + 1024u + 256u;   // + the per-CTA reservation and static shared memory
+    } else if (tree) {   // outcome-tree kernel (saim_mkp_tree.cu)
       const int lanes = (ctx->flags & SAIM_FLAG_MKP_L4) ? 4 : 2;
       uint32_t pw = 0;
       int wpc = 0;
@@ -492,6 +518,25 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
     a.mkp_prod = prod ? 1 : 0;
     wpc = std::max(1, std::min(wpc, prod ? ctx->max_wpc_prod : ctx->max_wpc));
     gx = ((R + 31) / 32 + wpc - 1) / wpc;
+  } else if (ctx->mkp_kind == 3) {
+    // speculative sub-warp kernel: the whole grid resident in one wave if registers and shared
+    // memory allow, with the fewest warps on the fullest SM (then the smallest CTAs: even spread);
+    // otherwise one CTA per SM and the fewest waves x warps per CTA
+    const int C = 32 / ctx->lanes;
+    const int warps_inst = (R + C - 1) / C;
+    long long best = -1;
+    for (int w = 1; w <= ctx->max_wpc; ++w) {
+      const long long ctas = (long long)((warps_inst + w - 1) / w) * ctx->n_inst;
+      const long long per_sm = (ctas + ctx->sm_count - 1) / ctx->sm_count;
+      const bool fit1 = (long long)ctx->spec_fixed + (long long)w * ctx->per_warp <= ctx->smem_sm &&
+                        w * 32LL * std::max(ctx->spec_regs, 1) <= 65536;
+      if (!fit1) break;
+      const bool fits = per_sm * ((long long)ctx->spec_fixed + (long long)w * ctx->per_warp) <= ctx->smem_sm &&
+                        per_sm * w * 32LL * std::max(ctx->spec_regs, 1) <= 65536 && per_sm * w <= 64 && per_sm <= 32;
+      const long long cost = fits ? per_sm * w : 1000000LL + per_sm * w;   // (not resident: per_sm = waves)
+      if (best < 0 || cost < best) { best = cost; wpc = w; }
+    }
+    gx = (warps_inst + wpc - 1) / wpc;
   } else {
     // one CTA per SM: spread each instance's warps over floor(SMs / n_inst) CTAs
     const int G = 32 / ctx->lanes;
@@ -524,6 +569,8 @@ extern "C" int saim_run(saim_ctx *ctx, uint64_t seed, int32_t rep0, int32_t R, i
       e = mkp_launch(a, ctx->n_inst, ctx->mm, wpc, prod ? ctx->per_warp_prod : ctx->per_warp, st, replay);
     else if (ctx->mkp_kind == 1)
       e = mkpt_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st, replay);
+    else if (ctx->mkp_kind == 3)
+      e = mkpx_launch(a, ctx->n_inst, ctx->mm, ctx->lanes, wpc, ctx->per_warp, st, replay);
     else
       e = mkps_launch(a, ctx->n_inst, ctx->mm, wpc, ctx->per_warp, st, replay);
   }

@@ -94,6 +94,21 @@ inline __host__ __device__ uint32_t mkpt_warp_bytes(int WN, int L, int MM) {
   return align16u((uint32_t)WN * G * 4u) + 128u * G * 4u + (uint32_t)MM * G * 8u;
 }
 
+// Speculative sub-warp MKP kernel (saim_mkp_spec.cuh, G lanes per chain): after the blob, the spin
+// table of all NS = 32 WN spins, one row of MM + 4 floats per spin (column A_{.i}, then c_p a_i,
+// -c_o c_i, |A_i|_1, E0_i); then per chain: x words [WN], Lambda [MM] int64, and one float4 per spin
+// (T_i = -c_o c_i - A_i . c_l Lambda and the error slope of this iteration; logit and logit
+// tolerance of the chain's current sweep).
+inline __host__ __device__ uint32_t mkpx_table_bytes(int WN, int MM) {
+  return (uint32_t)WN * 32u * ((uint32_t)MM * 4u + 16u);
+}
+inline __host__ __device__ uint32_t mkpx_chain_bytes(int WN, int MM) {
+  return align16u((uint32_t)WN * 4u) + (uint32_t)MM * 8u + (uint32_t)WN * 32u * 16u;
+}
+inline __host__ __device__ uint32_t mkpx_warp_bytes(int WN, int G, int MM) {
+  return (32u / (uint32_t)G) * mkpx_chain_bytes(WN, MM);
+}
+
 struct RunArgs {
   const unsigned char *blob;  // [n_inst][blob_bytes]
   const InstHdr *hdr;         // [n_inst]

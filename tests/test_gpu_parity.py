@@ -273,6 +273,9 @@ def _mkp(n, m, t, seed):
 # outcome tree with L = 2 and 4, row split over 2 lanes (honoured for M > 8; else the default)
 MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("lockstep_noprod", 2 | 64), ("tree_L2", 4), ("tree_L4", 8),
                 ("split2", 16)]
+# speculative sub-warp kernel with G = 2, 4, 8, 16 lanes per replica (instantiated for M <= 8)
+MKP_SPEC = [("spec2", 1024), ("spec4", 256), ("spec8", 512), ("spec16", 2048)]
+SPEC_LANES = {1024: 2, 256: 4, 512: 8, 2048: 16}
 
 
 @pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
@@ -288,12 +291,38 @@ def test_mkp_parity_small(P, n, m, variant):
     assert g["info"]["lanes_per_replica"] == want
 
 
+@pytest.mark.parametrize("variant", [v for _, v in MKP_SPEC], ids=[k for k, _ in MKP_SPEC])
+@pytest.mark.parametrize("n,m", [(7, 2), (30, 3), (33, 5), (64, 8), (100, 5), (131, 4)])
+def test_mkp_spec_parity_small(P, n, m, variant):
+    """The speculative sub-warp kernel for every G on small MKP instances with
+    ragged N (partial last block, partial last word, N > 128: two Philox groups) and R = 41
+    (a partial chain group in the last warp); T = 1 as well (fixed beta, no beta = 0 sweep)."""
+    p = _mkp(n, m, 0.5, 1)
+    g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=41, K=4, T=30, flags=variant)
+    assert g["info"]["kernel"] == 2 and g["info"]["lanes_per_replica"] == SPEC_LANES[variant]
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=9, K=3, T=1, flags=variant)
+
+
+def test_mkp_spec_needs_few_constraints(P):
+    p = _mkp(26, 10, 0.5, 1)
+    with pytest.raises(P.SaimError) as ei:
+        P.Solver(p.Q, p.c, p.A, p.b, si.paper_P(p, 5.0), 0.05, 50.0, flags=P.FLAG_MKP_SPEC4)
+    assert ei.value.code == P.SAIM_ESMEM
+
+
 @pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
 def test_mkp_parity_tiny_capacities(P, variant):
     p = _mkp(12, 3, 0.1, 2)
     p.b[:] = [1, 2, 3]
     run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=5, T=25, flags=variant)
     run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=3, T=1, flags=variant)  # fixed beta
+
+
+@pytest.mark.parametrize("variant", [v for _, v in MKP_SPEC], ids=[k for k, _ in MKP_SPEC])
+def test_mkp_spec_parity_tiny_capacities(P, variant):
+    p = _mkp(12, 3, 0.1, 2)
+    p.b[:] = [1, 2, 3]
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=32, K=5, T=25, flags=variant)
 
 
 def test_mkp_kernels_agree_on_counters(P):
@@ -304,7 +333,7 @@ def test_mkp_kernels_agree_on_counters(P):
     for p in (_mkp(100, 5, 0.5, 21), _mkp(60, 12, 0.5, 22)):
         Q, c, A, b = si.stack([p])
         runs = [gpu_run(P, Q, c, A, b, [si.paper_P(p, 5.0)], 0.05, 50.0, 3, 70, 6, 60, flags=v)
-                for _, v in MKP_VARIANTS]
+                for _, v in MKP_VARIANTS + (MKP_SPEC if p.M <= 8 else [])]
         for r in runs[1:]:
             for k in ["tr_x", "tr_f", "tr_feas", "tr_r", "tr_lam", "best_f", "best_k", "best_x", "n_feasible",
                       "final_x", "final_lam", "inst_best"]:
@@ -313,7 +342,7 @@ def test_mkp_kernels_agree_on_counters(P):
                 assert runs[0]["counters"][k] == r["counters"][k], k
 
 
-@pytest.mark.parametrize("variant", [0, 2], ids=["default", "lockstep"])
+@pytest.mark.parametrize("variant", [0, 2, 256, 512], ids=["default", "lockstep", "spec4", "spec8"])
 def test_mkp_parity_config3_sampled(P, variant):
     """Config 3 (three tightness variants in one launch) at full size; sampled replicas."""
     cfg = si.config_instances(3)
@@ -370,7 +399,7 @@ def test_degenerate_problems(P):
     m = _mkp(30, 3, 0.5, 4)
     m.A[1, :] = 0
     m.b[1] = 7
-    for v in (0, 2, 4, 8, 16):
+    for v in (0, 2, 4, 8, 16, 256, 512, 1024, 2048):
         run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=19, R=32, K=3, T=20, flags=v)
     # M > 8 with a row of zero weights in the second lane's half (row split)
     m = _mkp(30, 12, 0.5, 5)
