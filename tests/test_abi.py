@@ -69,7 +69,8 @@ def test_create_rejects_bad_input_without_gpu():
     with pytest.raises(P.SaimError) as ei:
         P.Solver(big, [[0, 0], [0, 0]], [[[1, 1], [1, 1]], [[1, 1], [1, 1]]], [[1, 1], [1, 1]], 1.0, 1.0, 1.0)
     assert ei.value.code == P.SAIM_EUNSUPPORTED                             # quadratic with M = 2
-    for bad in (256, P.FLAG_MKP_LOCKSTEP | P.FLAG_MKP_L2, P.FLAG_MKP_L2 | P.FLAG_MKP_L4, P.FLAG_MKP_SPLIT2 | P.FLAG_MKP_L4):
+    for bad in (8192, P.FLAG_MKP_LOCKSTEP | P.FLAG_MKP_L2, P.FLAG_MKP_L2 | P.FLAG_MKP_L4, P.FLAG_MKP_SPLIT2 | P.FLAG_MKP_L4,
+                P.FLAG_MKP_SPEC4 | P.FLAG_MKP_SPEC8, P.FLAG_MKP_SPEC8 | P.FLAG_MKP_L2):
         with pytest.raises(P.SaimError) as ei:                              # unknown / conflicting flags
             P.Solver(None, [0, 0], [[1, 1], [1, 0]], [3, 1], 1.0, 1.0, 1.0, flags=bad)
         assert ei.value.code == P.SAIM_EINVAL
