@@ -357,28 +357,36 @@ extern "C" int saim_create(const saim_problem *prob, const saim_params *par, sai
     const int MM = ctx->mm;
     const MkpLayout L = mkp_layout(n, MM);
     ctx->smem_bytes = (int)(L.bytes + ctx->per_warp);
-    // Default (measured on B200): outcome tree with L = 2 for M <= 8, the
-    // lockstep kernel for M > 8; the row split (M > 8) only on request.
+    // Default (measured on B200): the speculative sub-warp kernel with G = 8
+    // lanes per replica for M <= 8 (the outcome tree with L = 2 if it does not fit), the lockstep
+    // kernel for M > 8; the row split (M > 8) only on request.
     const int xmask = SAIM_FLAG_MKP_SPEC2 | SAIM_FLAG_MKP_SPEC4 | SAIM_FLAG_MKP_SPEC8 | SAIM_FLAG_MKP_SPEC16 | SAIM_FLAG_MKP_SPEC32;
-    const bool spec = (ctx->flags & xmask) != 0;
+    const int kmask = SAIM_FLAG_MKP_LOCKSTEP | SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4 | SAIM_FLAG_MKP_SPLIT2 | xmask;
+    bool spec = (ctx->flags & xmask) != 0 || (!(ctx->flags & kmask) && M <= 8);
+    if (spec) {   // speculative sub-warp kernel (saim_mkp_spec.cu)
+      const int G = (ctx->flags & SAIM_FLAG_MKP_SPEC2) ? 2 : (ctx->flags & SAIM_FLAG_MKP_SPEC4) ? 4
+                    : (ctx->flags & SAIM_FLAG_MKP_SPEC16) ? 16 : (ctx->flags & SAIM_FLAG_MKP_SPEC32) ? 32 : 8;
+      uint32_t tb = 0, pw = 0;
+      int wpc = 0;
+      if (mkpx_plan(M, ctx->N_max, smem_optin, MM, L.bytes, G, &tb, &pw, &wpc, &ctx->spec_regs) == 0) {
+        ctx->lanes = G;
+        ctx->mkp_kind = 3;
+        ctx->per_warp = pw;
+        ctx->max_wpc = wpc;
+        ctx->smem_bytes = (int)(L.bytes + tb + pw);
+        ctx->spec_fixed = L.bytes + tb + 1024u + 256u;   // + the per-CTA reservation and static shared memory
+      } else if (ctx->flags & xmask) {
+        delete ctx;
+        return fail(SAIM_ESMEM, "MKP speculative kernel (G=%d) has no instantiation for M=%d or does not fit shared memory", G, M);
+      } else {
+        spec = false;
+      }
+    }
     const bool tree = (ctx->flags & (SAIM_FLAG_MKP_L2 | SAIM_FLAG_MKP_L4)) ||
                       (!spec && !(ctx->flags & SAIM_FLAG_MKP_LOCKSTEP) && M <= 8);
     const bool split = !tree && !spec && MM >= 16 && (ctx->flags & SAIM_FLAG_MKP_SPLIT2);
-    if (spec) {   // speculative sub-warp kernel (saim_mkp_spec.cu)
-      const int G = (ctx->flags & SAIM_FLAG_MKP_SPEC2) ? 2 : (ctx->flags & SAIM_FLAG_MKP_SPEC4) ? 4
-                    : (ctx->flags & SAIM_FLAG_MKP_SPEC8) ? 8 : (ctx->flags & SAIM_FLAG_MKP_SPEC16) ? 16 : 32;
-      uint32_t tb = 0, pw = 0;
-      int wpc = 0;
-      if (mkpx_plan(M, ctx->N_max, smem_optin, MM, L.bytes, G, &tb, &pw, &wpc, &ctx->spec_regs) != 0) {
-        delete ctx;
-        return fail(SAIM_ESMEM, "MKP speculative kernel (G=%d) has no instantiation for M=%d or does not fit shared memory", G, M);
-      }
-      ctx->lanes = G;
-      ctx->mkp_kind = 3;
-      ctx->per_warp = pw;
-      ctx->max_wpc = wpc;
-      ctx->smem_bytes = (int)(L.bytes + tb + pw);
-      ctx->spec_fixed = L.bytes + tb + 1024u + 256u;   // + the per-CTA reservation and static shared memory
+    if (spec) {
+      // (planned above)
     } else if (tree) {   // outcome-tree kernel (saim_mkp_tree.cu)
       const int lanes = (ctx->flags & SAIM_FLAG_MKP_L4) ? 4 : 2;
       uint32_t pw = 0;

@@ -141,14 +141,9 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
   __syncthreads();
 
   const int gi = lane / G, ell = lane % G, gbase = gi * G;
-  // Spins are assigned to a chain's lanes in DESCENDING lane order (lane gbase + G-1 owns the
-  // block's first spin), so the first event in spin order is the highest set bit of a ballot.
-  const int so = G - 1 - ell;                          // this lane's spin within the block
-  uint32_t lanebit = 1u << lane;
   uint32_t gmsh = GM << gbase;                         // this chain's lanes
-  uint32_t before = gmsh & ~((lanebit << 1) - 1u);     // ... those whose spin comes before this lane's
-  // (opaque to the compiler: kept in registers instead of being recomputed in every round)
-  asm volatile("" : "+r"(lanebit), "+r"(gmsh), "+r"(before));
+  // (opaque to the compiler: kept in a register instead of being recomputed in every round)
+  asm volatile("" : "+r"(gmsh));
   const int wglob = blockIdx.x * (blockDim.x >> 5) + warp;
   if (wglob * C >= a.R) return;       // whole warp beyond R
   const int ridx = wglob * C + gi;
@@ -178,15 +173,10 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
   const uint32_t srho = ((uint32_t)s << 20) | (uint32_t)rho;
   const double bstep = (a.T >= 2) ? a.beta_max / (double)(a.T - 1) : a.beta_max;
   const int Wn = (n + 31) >> 5;
-  const int NB = (N + G - 1) / G;                      // blocks per sweep
   const int WNi = (N + 31) >> 5, NG = (N + 127) >> 7;  // words / 128-spin Philox groups of this instance
-  // lanes of the last block that own a spin (the top N - (NB-1) G lanes of the chain)
-  uint32_t og_last = (N - (NB - 1) * G >= G ? GM : (GM & ~(GM >> ((N - (NB - 1) * G) & 31)))) << gbase;
-  int i0_last = (NB - 1) * G;                          // first spin of the sweep's last block
-  asm volatile("" : "+r"(og_last), "+r"(i0_last));
-  // shared-window byte addresses: row of this lane's spin in block 0, its table entry, the x words
-  uint32_t rowbase = (uint32_t)__cvta_generic_to_shared(trow + so * RS);
-  uint32_t ktbase = (uint32_t)__cvta_generic_to_shared(kt + so);
+  // shared-window byte addresses: the spin table, this chain's per-spin table and x words
+  uint32_t rowbase = (uint32_t)__cvta_generic_to_shared(trow);
+  uint32_t ktbase = (uint32_t)__cvta_generic_to_shared(kt);
   uint32_t xwbase = (uint32_t)__cvta_generic_to_shared(xw);
   asm volatile("" : "+r"(rowbase), "+r"(ktbase), "+r"(xwbase));
 
@@ -243,21 +233,25 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
     }
     __syncwarp();
 
-    // ---- chain cursor and the registers of the current block ----
-    int t = 0, i0 = 0;                                 // sweep, first spin of the block
+    // ---- chain state (identical in the chain's lanes) and this lane's current spin ----
+    // Sliding window: the chain's G lanes always hold its next G spins that are not final yet;
+    // spin i belongs to lane i mod G, so a lane whose spin became final moves on to spin i + G.
+    int t = 0, w0 = 0;                                 // sweep, first spin that is not final
     bool done = false, wrapf = false;                  // wrapf: sweep finished, the next one not yet entered
     double beta = (a.T >= 2) ? 0.0 : a.beta_max;
     float bf = (float)beta, tb = -bf * twocp;
-    uint32_t og = 0;                                   // lanes of the chain whose spin is not yet final
-    uint32_t xcur = 0;                                 // x word of the block (identical in the chain's lanes)
-    uint32_t xwp = xwbase;                             // (shared-window address of the block's x word)
-    uint32_t rowp = rowbase;                           // ... of this lane's spin's row of the table
+    int ime = ell - G;                                 // this lane's spin (>= N: none left in this sweep)
+    bool open = false;                                 // ... exists and is not final
     float a_[MA];
-    // signed by sg = 1 - 2 x_i (x_i the spin's value at block load): zs = sg z, ls = sg logit
+    // signed by sg = 1 - 2 x_i (x_i the spin's value when the lane took it): zs = sg z, ls = sg logit
     float tbs = 0.f, zbs = 0.f, ls = 0.f, satT = 0.f, certT = 0.f, sg = 1.0f;
 
-    auto load_block = [&]() {
-      rowp = rowbase + (uint32_t)(i0 * (RS * 4));
+    // this lane takes spin ime + G (if the sweep has one)
+    auto next_spin = [&]() {
+      ime += G;
+      open = ime < N && !done;
+      const int il = open ? ime : 0;                   // (a lane without a spin loads row 0, unused)
+      const uint32_t rowp = rowbase + (uint32_t)(il * (RS * 4));
       float cpa;
 #pragma unroll
       for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
@@ -269,10 +263,9 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
         if (CPA / 4 == m4) cpa = (CPA % 4 == 1) ? av.y : ((CPA % 4 == 2) ? av.z : av.w);
       }
       if (CPA == MM) cpa = lds32f(rowp + 4u * MM);
-      const float4 kv = lds128(ktbase + (uint32_t)(i0 * 16));
-      xwp = xwbase + (uint32_t)((i0 >> 5) * 4);
-      xcur = lds32u(xwp);
-      sg = ((xcur >> ((i0 + so) & 31)) & 1u) ? -1.0f : 1.0f;
+      const float4 kv = lds128(ktbase + (uint32_t)(il * 16));
+      const uint32_t xb = (lds32u(xwbase + (uint32_t)((il >> 5) * 4)) >> (il & 31)) & 1u;
+      sg = xb ? -1.0f : 1.0f;
       // F = T_i - c_p a_i sg - 2 c_p (A_i . r);  zs = sg beta F = fma(sg tb, A_i . r, bf (sg T_i - c_p a_i))
       zbs = bf * fmaf(sg, kv.x, -cpa);
       tbs = sg * tb;
@@ -280,13 +273,12 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
       const float e = bf * kv.y;
       satT = e + kSatThr;
       certT = fmaf(e, 1.0001f, kv.w);
-      og = (i0 == i0_last) ? og_last : gmsh;
     };
 
     // fp64 second level (and, in the replay instantiation, the double-double third level) for
     // this lane's spin in the current state: returns x | uncertified << 1.
     auto slow = [&]() -> int {
-      const int i = i0 + so;
+      const int i = ime;
       const uint32_t wd = word_of_x(key, i, t, k, srho);
       double drd = 0.0, dld = 0.0, a2 = 0.0;
 #pragma unroll
@@ -312,15 +304,11 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
       return rs;
     };
 
-    load_block();
-
-    // ---- rounds ----
-    // r += delta (column of warp lane jl's spin), x bit toggled (called by all lanes of the chain)
-    auto apply_flip = [&](int jl, bool doit) {
-      const int dj = lane - jl;                        // (spins ascend as lanes descend)
-      const uint32_t cj = rowp + (uint32_t)(dj * (RS * 4));
-      const uint32_t xbit = 1u << ((i0 + so + dj) & 31);
-      const float dl = doit ? ((xcur & xbit) ? -1.0f : 1.0f) : 0.0f;   // delta = 1 - 2 x_j (0: fma(0, a, r) = r)
+    // spin iev of the chain flips (doit) from x = xold: r += delta A_iev, x bit toggled in the
+    // chain's x words (called by all lanes of the chain; all store the same word)
+    auto apply_flip = [&](int iev, bool xold, bool doit) {
+      const uint32_t cj = rowbase + (uint32_t)(iev * (RS * 4));
+      const float dl = doit ? (xold ? -1.0f : 1.0f) : 0.0f;       // delta = 1 - 2 x_j (0: fma(0, a, r) = r)
 #pragma unroll
       for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
         const float4 av = lds128(cj + 16u * m4);
@@ -329,10 +317,14 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
         if (4 * m4 + 2 < MA) r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
         if (4 * m4 + 3 < MA) r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
       }
-      xcur ^= doit ? xbit : 0u;
-      sts32u(xwp, xcur);                               // (every lane of the chain stores the same word)
+      const uint32_t xa = xwbase + (uint32_t)((iev >> 5) * 4);
+      sts32u(xa, lds32u(xa) ^ (doit ? (1u << (iev & 31)) : 0u));
       c_flips += doit ? 1u : 0u;
     };
+
+    next_spin();
+
+    // ---- rounds ----
 #pragma unroll 1
     for (;;) {
       float p0 = 0.f, p1 = 0.f;
@@ -348,40 +340,46 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
       // need: not certified in fp32 (ties z = 0, d = 0 included)
       const bool flip = (sat ? zs : ds) > 0.0f;
       const bool need = !sat && !(fabsf(ds) > certT);
-      const bool open = (og & lanebit) != 0u;
-      const uint32_t evw = __ballot_sync(kFullX, open && (flip || need));   // events
-      const uint32_t cfw = __ballot_sync(kFullX, open && flip && !need);    // certified flips
-      // final this round: the open lanes up to the chain's first event; the event lane itself if
-      // its flip is certified (an uncertified one is settled in the rare path below)
-      const bool fin = open && (evw & before) == 0u && !need;
-      c_unif += (fin && !sat) ? 1u : 0u;                                    // (this lane's spin drew u)
-      og = __ballot_sync(kFullX, open && !fin) & gmsh;
-      const uint32_t evg = evw & gmsh;
-      const int jl = evg ? 31 - __clz(evg) : lane;     // the chain's first event lane
-      const bool cflip = ((cfw >> jl) & 1u) != 0u && evg != 0u;
-      apply_flip(jl, cflip);
-      // rare: the chain's first event is an uncertified decision, or the chain finished its sweep
-      // in the previous round (it idles this round: og = 0)
-      const bool nfirst = evg != 0u && !cflip;
+      // The chain's first event (flip or uncertified decision) in spin order: the window starts at
+      // lane w0 mod G and wraps around, so the chain's ballot bits are rotated by that much.
+      const uint32_t evw = __ballot_sync(kFullX, open && (flip || need));
+      const uint32_t ndw = __ballot_sync(kFullX, open && need);
+      const uint32_t xnw = __ballot_sync(kFullX, sg < 0.0f);
+      const uint32_t e = (evw >> gbase) & GM;
+      const bool hasev = e != 0u;
+      const int s0 = w0 & (G - 1);
+      uint32_t rot;
+      if constexpr (G == 32) rot = __funnelshift_r(e, e, s0);
+      else rot = (e | (e << G)) >> s0;
+      const int kk = __ffs(rot) - 1;
+      const int iev = hasev ? w0 + kk : 0;             // the event's spin (0: none, row 0 is read and unused)
+      const int jl = gbase + ((s0 + kk) & (G - 1));    // ... and lane
+      const bool nfirst = hasev && ((ndw >> jl) & 1u) != 0u;   // an uncertified decision: rare path
+      const bool xold = ((xnw >> jl) & 1u) != 0u;
+      // final this round: the open lanes up to the event, the event itself if its flip is certified
+      bool fin = open && (!hasev || ime < iev + (nfirst ? 0 : 1));
+      c_unif += (fin && !sat) ? 1u : 0u;               // (this lane's spin drew u)
+      apply_flip(iev, xold, hasev && !nfirst);
+      w0 = hasev ? iev + (nfirst ? 0 : 1) : w0 + G;
       if (__any_sync(kFullX, nfirst || wrapf)) {
         bool sflip = false;
-        if (nfirst && lane == jl) {
+        if (nfirst && ime == iev && open) {
           ++c_fp64;
           const int rs = slow();
           if (rs & 2) ++c_unc;
           sflip = (rs & 1) != (sg < 0.0f ? 1 : 0);
           ++c_unif;                                    // (not saturated: it drew u)
+          fin = true;                                  // settled now
         }
         const bool gflip = (__ballot_sync(kFullX, sflip) & gmsh) != 0u;
         if (nfirst) {
-          apply_flip(jl, gflip);
-          og &= ~(1u << jl);                           // the event lane is final now
+          apply_flip(iev, xold, gflip);
+          w0 = iev + 1;
         }
         if (__any_sync(kFullX, wrapf)) {
           if (wrapf) {
             ++t;
             done = t == a.T;
-            i0 = -G;                                   // (its block 0 is loaded at the end of this round)
           }
           uint32_t fw = __ballot_sync(kFullX, wrapf && !done);
           while (fw) {
@@ -396,15 +394,15 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
             beta = bstep * (double)t;                  // (T >= 2 here: T = 1 is done after sweep 0)
             bf = (float)beta;
             tb = -bf * twocp;
+            w0 = 0;
+            ime = ell - G;                             // (takes spin ell just below)
+            fin = true;
           }
           if (__all_sync(kFullX, done)) break;
         }
       }
-      if (og == 0u && !done && !wrapf) {                // block final: next block, or the sweep is finished
-        i0 += G;
-        if (i0 > i0_last) wrapf = true;
-        else load_block();
-      }
+      if (fin) next_spin();
+      if (w0 >= N && !done) wrapf = true;              // sweep finished (every lane has open = false)
     }
     __syncwarp();
 

@@ -269,13 +269,13 @@ def _mkp(n, m, t, seed):
     return si.mkp(n, m, t, [88, n, m, seed])
 
 
-# MKP kernel variants: default (outcome tree L = 2 for M <= 8, lockstep for M > 8), lockstep,
+# MKP kernel variants: default (speculative sub-warp kernel G = 8 for M <= 8, lockstep for M > 8), lockstep,
 # outcome tree with L = 2 and 4, row split over 2 lanes (honoured for M > 8; else the default)
 MKP_VARIANTS = [("default", 0), ("lockstep", 2), ("lockstep_noprod", 2 | 64), ("tree_L2", 4), ("tree_L4", 8),
                 ("split2", 16)]
-# speculative sub-warp kernel with G = 2, 4, 8, 16 lanes per replica (instantiated for M <= 8)
-MKP_SPEC = [("spec2", 1024), ("spec4", 256), ("spec8", 512), ("spec16", 2048)]
-SPEC_LANES = {1024: 2, 256: 4, 512: 8, 2048: 16}
+# speculative sub-warp kernel with G = 2, 4, 8, 16, 32 lanes per replica (instantiated for M <= 8)
+MKP_SPEC = [("spec2", 1024), ("spec4", 256), ("spec8", 512), ("spec16", 2048), ("spec32", 4096)]
+SPEC_LANES = {1024: 2, 256: 4, 512: 8, 2048: 16, 4096: 32}
 
 
 @pytest.mark.parametrize("variant", [v for _, v in MKP_VARIANTS], ids=[k for k, _ in MKP_VARIANTS])
@@ -286,7 +286,7 @@ def test_mkp_parity_small(P, n, m, variant):
     p = _mkp(n, m, 0.5, 1)
     g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=12, R=40, K=4, T=30, flags=variant)
     assert g["info"]["kernel"] == 2
-    default = 2 if m <= 8 else 1
+    default = 8 if m <= 8 else 1          # speculative sub-warp kernel (G = 8) / lockstep
     want = {0: default, 2: 1, 66: 1, 4: 2, 8: 4, 16: 2}[variant]
     assert g["info"]["lanes_per_replica"] == want
 
@@ -342,7 +342,7 @@ def test_mkp_kernels_agree_on_counters(P):
                 assert runs[0]["counters"][k] == r["counters"][k], k
 
 
-@pytest.mark.parametrize("variant", [0, 2, 256, 512], ids=["default", "lockstep", "spec4", "spec8"])
+@pytest.mark.parametrize("variant", [0, 2, 4, 256], ids=["default", "lockstep", "tree_L2", "spec4"])
 def test_mkp_parity_config3_sampled(P, variant):
     """Config 3 (three tightness variants in one launch) at full size; sampled replicas."""
     cfg = si.config_instances(3)
@@ -399,7 +399,7 @@ def test_degenerate_problems(P):
     m = _mkp(30, 3, 0.5, 4)
     m.A[1, :] = 0
     m.b[1] = 7
-    for v in (0, 2, 4, 8, 16, 256, 512, 1024, 2048):
+    for v in (0, 2, 4, 8, 16, 256, 512, 1024, 2048, 4096):
         run_both(P, [m], [si.paper_P(m, 5.0)], 0.05, 50.0, seed=19, R=32, K=3, T=20, flags=v)
     # M > 8 with a row of zero weights in the second lane's half (row split)
     m = _mkp(30, 12, 0.5, 5)
