@@ -340,28 +340,42 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
       // need: not certified in fp32 (ties z = 0, d = 0 included)
       const bool flip = (sat ? zs : ds) > 0.0f;
       const bool need = !sat && !(fabsf(ds) > certT);
-      // The chain's first event (flip or uncertified decision) in spin order: the window starts at
-      // lane w0 mod G and wraps around, so the chain's ballot bits are rotated by that much.
-      const uint32_t evw = __ballot_sync(kFullX, open && (flip || need));
-      const uint32_t ndw = __ballot_sync(kFullX, open && need);
-      const uint32_t xnw = __ballot_sync(kFullX, sg < 0.0f);
-      const uint32_t e = (evw >> gbase) & GM;
-      const bool hasev = e != 0u;
-      const int s0 = w0 & (G - 1);
-      uint32_t rot;
-      if constexpr (G == 32) rot = __funnelshift_r(e, e, s0);
-      else rot = (e | (e << G)) >> s0;
-      const int kk = __ffs(rot) - 1;
-      const int iev = hasev ? w0 + kk : 0;             // the event's spin (0: none, row 0 is read and unused)
-      const int jl = gbase + ((s0 + kk) & (G - 1));    // ... and lane
-      const bool nfirst = hasev && ((ndw >> jl) & 1u) != 0u;   // an uncertified decision: rare path
-      const bool xold = ((xnw >> jl) & 1u) != 0u;
-      // final this round: the open lanes up to the event, the event itself if its flip is certified
-      bool fin = open && (!hasev || ime < iev + (nfirst ? 0 : 1));
-      c_unif += (fin && !sat) ? 1u : 0u;               // (this lane's spin drew u)
-      apply_flip(iev, xold, hasev && !nfirst);
-      w0 = hasev ? iev + (nfirst ? 0 : 1) : w0 + G;
-      if (__any_sync(kFullX, nfirst || wrapf)) {
+      // The chain's first event in spin order: the window starts at lane w0 mod G and wraps
+      // around, so the chain's ballot bits are rotated by that much before the first set bit is
+      // taken.  Returns the event's spin (0 if none: row 0 is then read and unused) and lane.
+      auto first_event = [&](uint32_t evw, bool &hasev, int &iev, int &jl) {
+        const uint32_t e = (evw >> gbase) & GM;
+        hasev = e != 0u;
+        const int s0 = w0 & (G - 1);
+        uint32_t rot;
+        if constexpr (G == 32) rot = __funnelshift_r(e, e, s0);
+        else rot = (e | (e << G)) >> s0;
+        const int kk = __ffs(rot) - 1;
+        iev = hasev ? w0 + kk : 0;
+        jl = gbase + ((s0 + kk) & (G - 1));
+      };
+      const uint32_t cfw = __ballot_sync(kFullX, open && flip && !need);     // certified flips
+      bool hasev, fin;
+      int iev, jl;
+      if (!__any_sync(kFullX, (open && need) || wrapf)) {
+        // ---- common round: every open decision of the warp is certified ----
+        first_event(cfw, hasev, iev, jl);
+        // final: the open lanes up to the flip (all of them if there is none)
+        fin = open && (!hasev || ime <= iev);
+        c_unif += (fin && !sat) ? 1u : 0u;             // (this lane's spin drew u)
+        const float dlj = __shfl_sync(kFullX, sg, jl);  // delta = 1 - 2 x of the flipping spin
+        apply_flip(iev, dlj < 0.0f, hasev);
+        w0 = hasev ? iev + 1 : w0 + G;
+      } else {
+        // ---- rare round: some open decision is not certified in fp32 (it is an event too: if it
+        // is its chain's first, it is settled on the slow path), or a chain finished its sweep in
+        // the previous round (it idles this round) ----
+        first_event(__ballot_sync(kFullX, open && (flip || need)), hasev, iev, jl);
+        const uint32_t ndw = __ballot_sync(kFullX, open && need);
+        const bool nfirst = hasev && ((ndw >> jl) & 1u) != 0u;
+        const bool xold = __shfl_sync(kFullX, sg, jl) < 0.0f;
+        fin = open && (!hasev || ime < iev + (nfirst ? 0 : 1));
+        c_unif += (fin && !sat) ? 1u : 0u;
         bool sflip = false;
         if (nfirst && ime == iev && open) {
           ++c_fp64;
@@ -372,10 +386,8 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
           fin = true;                                  // settled now
         }
         const bool gflip = (__ballot_sync(kFullX, sflip) & gmsh) != 0u;
-        if (nfirst) {
-          apply_flip(iev, xold, gflip);
-          w0 = iev + 1;
-        }
+        apply_flip(iev, xold, hasev && (!nfirst || gflip));
+        w0 = hasev ? iev + 1 : w0 + G;
         if (__any_sync(kFullX, wrapf)) {
           if (wrapf) {
             ++t;

@@ -18,10 +18,15 @@ def main():
     ap.add_argument("--R", type=int, default=None)
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--inst", type=int, default=None, help="run only this instance of the config")
     a = ap.parse_args()
     import torch
     cfg = si.config_instances(a.config)
-    sol = P.Solver.from_config(cfg, flags=a.flags)
+    if a.inst is not None:
+        p = cfg.instances[a.inst]
+        sol = P.Solver(p.Q, p.c, p.A, p.b, cfg.P[a.inst], cfg.eta, cfg.beta_max, flags=a.flags)
+    else:
+        sol = P.Solver.from_config(cfg, flags=a.flags)
     R, K, T = a.R or cfg.R, a.K or cfg.K, a.T or cfg.T
     out = sol.alloc_outputs(R, K)
     for i in range(a.reps):
