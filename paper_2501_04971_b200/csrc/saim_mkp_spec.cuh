@@ -141,6 +141,7 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
   __syncthreads();
 
   const int gi = lane / G, ell = lane % G, gbase = gi * G;
+  const int sl = G - 1 - ell;                          // this lane's spins are i = sl (mod G)
   uint32_t gmsh = GM << gbase;                         // this chain's lanes
   // (opaque to the compiler: kept in a register instead of being recomputed in every round)
   asm volatile("" : "+r"(gmsh));
@@ -235,12 +236,12 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
 
     // ---- chain state (identical in the chain's lanes) and this lane's current spin ----
     // Sliding window: the chain's G lanes always hold its next G spins that are not final yet;
-    // spin i belongs to lane i mod G, so a lane whose spin became final moves on to spin i + G.
+    // spin i belongs to lane G-1 - i mod G, so a lane whose spin became final moves on to spin i + G.
     int t = 0, w0 = 0;                                 // sweep, first spin that is not final
     bool done = false, wrapf = false;                  // wrapf: sweep finished, the next one not yet entered
     double beta = (a.T >= 2) ? 0.0 : a.beta_max;
     float bf = (float)beta, tb = -bf * twocp;
-    int ime = ell - G;                                 // this lane's spin (>= N: none left in this sweep)
+    int ime = sl - G;                                  // this lane's spin (>= N: none left in this sweep)
     bool open = false;                                 // ... exists and is not final
     float a_[MA];
     // signed by sg = 1 - 2 x_i (x_i the spin's value when the lane took it): zs = sg z, ls = sg logit
@@ -273,6 +274,10 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
       const float e = bf * kv.y;
       satT = e + kSatThr;
       certT = fmaf(e, 1.0001f, kv.w);
+      if (!open) {                                     // no spin: certified "saturated, no flip" in every round
+        tbs = 0.0f;
+        zbs = -3.0e38f;
+      }
     };
 
     // fp64 second level (and, in the replay instantiation, the double-double third level) for
@@ -335,29 +340,34 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
       }
       const float zs = fmaf(tbs, p0 + p1, zbs);
       const float ds = zs - ls;
+      // Certified decision, signed (sg z, sg (z - logit)): the spin flips <=> sg z > 0 if
+      // saturated, sg (z - logit) > 0 otherwise.  cf: a certified flip (saturated towards the
+      // flip, or unsaturated with sg (z - logit) beyond the fp32 band); need: unsaturated and
+      // inside the band (ties z = 0, d = 0 included): not certified in fp32.  A lane without a
+      // spin has zs = -3e38: saturated, no flip.
       const bool sat = fabsf(zs) > satT;
-      // certified decision, signed: the spin flips <=> sg z > 0 (saturated) / sg (z - logit) > 0;
-      // need: not certified in fp32 (ties z = 0, d = 0 included)
-      const bool flip = (sat ? zs : ds) > 0.0f;
+      const bool cf = zs > satT || (ds > certT && !sat);
       const bool need = !sat && !(fabsf(ds) > certT);
-      // The chain's first event in spin order: the window starts at lane w0 mod G and wraps
-      // around, so the chain's ballot bits are rotated by that much before the first set bit is
-      // taken.  Returns the event's spin (0 if none: row 0 is then read and unused) and lane.
+      // The chain's first event in spin order.  Spin i belongs to the chain's lane G-1 - i mod G
+      // (descending), the window starts at spin w0 and wraps around the lanes: the chain's ballot
+      // bits rotated left by w0 mod G have the window's k-th spin at bit G-1-k, so the first event
+      // is the highest set bit (one FLO).  Returns the event's spin (0 if none: row 0 is then read
+      // and unused) and lane.
       auto first_event = [&](uint32_t evw, bool &hasev, int &iev, int &jl) {
         const uint32_t e = (evw >> gbase) & GM;
         hasev = e != 0u;
         const int s0 = w0 & (G - 1);
         uint32_t rot;
-        if constexpr (G == 32) rot = __funnelshift_r(e, e, s0);
-        else rot = (e | (e << G)) >> s0;
-        const int kk = __ffs(rot) - 1;
+        if constexpr (G == 32) rot = __funnelshift_l(e, e, s0);
+        else rot = ((e | (e << G)) >> (G - s0)) & GM;
+        const int kk = __clz(rot) - (32 - G);
         iev = hasev ? w0 + kk : 0;
-        jl = gbase + ((s0 + kk) & (G - 1));
+        jl = gbase + G - 1 - ((s0 + kk) & (G - 1));
       };
-      const uint32_t cfw = __ballot_sync(kFullX, open && flip && !need);     // certified flips
+      const uint32_t cfw = __ballot_sync(kFullX, cf);                        // certified flips
       bool hasev, fin;
       int iev, jl;
-      if (!__any_sync(kFullX, (open && need) || wrapf)) {
+      if (!__any_sync(kFullX, need || wrapf)) {
         // ---- common round: every open decision of the warp is certified ----
         first_event(cfw, hasev, iev, jl);
         // final: the open lanes up to the flip (all of them if there is none)
@@ -370,8 +380,8 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
         // ---- rare round: some open decision is not certified in fp32 (it is an event too: if it
         // is its chain's first, it is settled on the slow path), or a chain finished its sweep in
         // the previous round (it idles this round) ----
-        first_event(__ballot_sync(kFullX, open && (flip || need)), hasev, iev, jl);
-        const uint32_t ndw = __ballot_sync(kFullX, open && need);
+        first_event(__ballot_sync(kFullX, cf || need), hasev, iev, jl);
+        const uint32_t ndw = __ballot_sync(kFullX, need);
         const bool nfirst = hasev && ((ndw >> jl) & 1u) != 0u;
         const bool xold = __shfl_sync(kFullX, sg, jl) < 0.0f;
         fin = open && (!hasev || ime < iev + (nfirst ? 0 : 1));
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__((G == 32 ? 672 : (G == 16 ? 352 : 512)), (G ==
             bf = (float)beta;
             tb = -bf * twocp;
             w0 = 0;
-            ime = ell - G;                             // (takes spin ell just below)
+            ime = sl - G;                              // (takes spin sl just below)
             fin = true;
           }
           if (__all_sync(kFullX, done)) break;
