@@ -2,24 +2,24 @@
 // (MKP; BASELINE.json config 3).  sm_100a.
 //
 // Mapping: G = 2..32 adjacent LANES = one replica (chain), C = 32/G chains per
-// warp.  Lane l of a chain owns spin bG + l of the chain's current block b of G consecutive spins
-// (items and slack bits alike: a slack bit q of row m is the column 2^q e_m, built into a per-CTA
-// spin table).  One ROUND evaluates, for every lane, the decision of its spin on the chain's
-// current state; the first lane (in spin order) whose decision flips is the chain's next state
-// change: the lanes before it are final, the flip is applied to r (replicated in the chain's
-// lanes), and the lanes after it are evaluated again in the next round with the same
-// counter-based uniforms -- the sequential sweep of Eq. 9-10, bit for bit.
-// A round without a flip finalises the block and the chain moves to the next one.  The chains of
-// a warp are NOT synchronised: each has its own block, position and sweep index, so a chain
-// takes exactly (blocks + flips) rounds per sweep whatever its neighbours do; they meet again at
-// the end of the anneal (readout, Lagrange step).  The logits of a chain's sweep are drawn by
-// all 32 lanes of the warp together when that chain enters the sweep.
+// warp.  The chain's lanes form a sliding window over the sweep: they always hold its next G spins
+// that are not final yet (spin i belongs to lane G-1 - i mod G; items and slack bits alike: a slack
+// bit q of row m is the column 2^q e_m, built into a per-CTA spin table).  One ROUND evaluates, for
+// every lane, the decision of its spin on the chain's current state; the first lane in spin order
+// whose decision flips is the chain's next state change: the lanes up to it are final and move on
+// to their next spins, the flip is applied to r (replicated in the chain's lanes), and the lanes
+// after it are evaluated again in the next round with the same counter-based uniforms -- the
+// sequential sweep of Eq. 9-10, bit for bit.  A round without a flip finalises
+// all G lanes.  The chains of a warp are NOT synchronised: each has its own window position and
+// sweep index, so a chain takes exactly (flips + flip-free runs of G spins) rounds per sweep
+// whatever its neighbours do; they meet again at the end of the anneal (readout, Lagrange step).
+// The logits of a chain's sweep are drawn by all 32 lanes of the warp together when that chain
+// enters the sweep.
 //
 // Why: config 3 has 6,144 chains.  Lane-per-chain (lockstep) makes 192 warps -- one per SMSP on a
 // third of the GPU -- and a chain's decision then costs its ~100 warp-instructions at the IPC of
-// a lone warp; the outcome trees (L lanes per chain) pay 2^l combinations.  Here a decision of a
-// chain costs one round of ~80 warp-instructions shared by C chains and G lanes of work, and a
-// chain's latency per sweep is (blocks + flips) rounds of ~90 cycles.
+// a lone warp; the outcome trees (L lanes per chain) pay 2^l combinations.  Here a round of ~105
+// warp-instructions is shared by C chains and finalises ~4 spins of each.
 //
 // Arithmetic and certification are those of the lockstep kernel (saim_mkp.cuh): r exact integers
 // in fp32, the field F_i = -c_o c_i - c_p a_i (1 - 2x_i) - 2 c_p (A_i . r) - (A_i . c_l Lambda)
