@@ -81,10 +81,12 @@ typedef struct {
  * (DESIGN.md "Exact early exit").  Results are bit-identical either way. */
 #define SAIM_FLAG_NO_FREEZE_EXIT 1
 /* Kernel selection for linear objectives with M >= 2 constraints (MKP).  Default: the
- * outcome-tree kernel with L = 2 lanes per replica for M <= 8, the lane-per-replica lockstep
+ * speculative sub-warp kernel with G = 8 lanes per replica for M <= 8 (SAIM_FLAG_MKP_SPEC8 below;
+ * the outcome tree with L = 2 if it does not fit shared memory), the lane-per-replica lockstep
  * kernel for M > 8 (the faster one on B200 for each).  These flags force the lockstep kernel,
  * the outcome tree with a given L, or the row-split kernel (each replica's constraint rows over
- * 2 lanes; honoured for M > 8 only).  At most one may be set.  All give identical results. */
+ * 2 lanes; honoured for M > 8 only).  At most one kernel-selection flag may be set.  All give
+ * identical results. */
 #define SAIM_FLAG_MKP_LOCKSTEP 2
 #define SAIM_FLAG_MKP_L2 4
 #define SAIM_FLAG_MKP_L4 8
@@ -99,10 +101,11 @@ typedef struct {
  * uncertified there, so it is re-decided at the double-double level (MKP: at once; QKP: by the
  * exact replay of the whole replica).  Results are identical either way; only slower. */
 #define SAIM_FLAG_TEST_REPLAY 128
-/* MKP, M <= 8: the speculative sub-warp kernel with G = 2, 4, 8, 16 or 32 lanes per replica (each
- * lane owns one spin of the replica's current block of G spins; the first flipping lane of a round
- * is applied and the later lanes are re-evaluated: DESIGN.md 6.5).  Counts as a kernel-selection
- * flag (at most one of these and the four above).  SAIM_ESMEM if M > 8.  Identical results. */
+/* MKP, M <= 8: the speculative sub-warp kernel with G = 2, 4, 8, 16 or 32 lanes per replica (the
+ * lanes hold the replica's next G spins that are not final; the first flipping lane of a round is
+ * applied and the later lanes are re-evaluated: DESIGN.md 6.5).  Kernel-selection flags (at most
+ * one of these and the four above).  SAIM_ESMEM if M > 8 or the tables do not fit.  Identical
+ * results. */
 #define SAIM_FLAG_MKP_SPEC2 1024
 #define SAIM_FLAG_MKP_SPEC4 256
 #define SAIM_FLAG_MKP_SPEC8 512
@@ -137,7 +140,8 @@ typedef struct {
   int32_t n_spins_max;     /* max over instances of N = n + sum_k q_k */
   int32_t words_items;     /* Wn = ceil(n/32) */
   int32_t words_full;      /* WN = ceil(N_max/32) */
-  int32_t kernel;          /* 1 = QKP warp-per-replica kernel (M <= 1), 2 = MKP lane-group kernel */
+  int32_t kernel;          /* 1 = QKP warp-per-replica kernel (M <= 1), 2 = MKP kernels (lanes_per_replica: 1 lockstep,
+                            * 2/4 outcome tree or row split, 2..32 speculative sub-warp) */
   int32_t smem_bytes;      /* dynamic shared memory per CTA */
   int32_t q_bytes;         /* bytes per stored Q entry (1 or 2), 0 if no Q */
   int32_t lanes_per_replica;
