@@ -303,6 +303,25 @@ def test_mkp_spec_parity_small(P, n, m, variant):
     run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=13, R=9, K=3, T=1, flags=variant)
 
 
+@pytest.mark.parametrize("variant", [0, 256, 2048], ids=["default_spec8", "spec4", "spec16"])
+def test_mkp_spec_edge_cases(P, variant):
+    """Edge cases of the speculative sub-warp kernel: N > 256 (three Philox groups, a spin table of
+    more than 8 words), T = 2 (only the beta = 0 sweep and beta_max), K = 1, the penalty method
+    (eta = 0), no penalty (P = 0), a huge beta_max (every decision saturates after the first
+    sweeps), a single replica, and a batch of two instances with different N in one launch."""
+    big = _mkp(300, 4, 0.5, 41)
+    run_both(P, [big], [si.paper_P(big, 5.0)], 0.05, 50.0, seed=31, R=9, K=2, T=12, flags=variant)
+    p = _mkp(45, 6, 0.5, 42)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=32, R=17, K=3, T=2, flags=variant)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=33, R=17, K=1, T=1, flags=variant)
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.0, 50.0, seed=34, R=8, K=3, T=20, flags=variant)      # eta = 0
+    run_both(P, [p], [0.0], 0.05, 50.0, seed=35, R=8, K=3, T=20, flags=variant)                    # P = 0
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 1e6, seed=36, R=8, K=3, T=20, flags=variant)      # saturated
+    run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=37, R=1, K=4, T=30, flags=variant)     # one replica
+    q = _mkp(45, 6, 0.25, 43)
+    run_both(P, [p, q], [si.paper_P(p, 5.0), si.paper_P(q, 5.0)], 0.05, 50.0, seed=38, R=13, K=3, T=25, flags=variant)
+
+
 def test_mkp_spec_needs_few_constraints(P):
     p = _mkp(26, 10, 0.5, 1)
     with pytest.raises(P.SaimError) as ei:
