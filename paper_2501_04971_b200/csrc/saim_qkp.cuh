@@ -53,6 +53,15 @@ __constant__ uint32_t kDivMagic[33] = {
     0,     65536, 32768, 21846, 16384, 13108, 10923, 9363, 8192, 7282, 6554, 5958, 5462, 5042, 4682, 4370, 4096,
     3856,  3641,  3450,  3277,  3121,  2979,  2850,  2731, 2622, 2521, 2428, 2341, 2260, 2185, 2115, 2048};
 
+// Shared-memory word by 32-bit shared-window address (apply_flip keeps the Q base as such an
+// address: through a generic pointer the compiler rebuilt the window base -- S2UR/UMOV/UIADD3/ULEA
+// -- on every flip).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t sel4(const uint4 &u, int i) {
   return i == 0 ? u.x : (i == 1 ? u.y : (i == 2 ? u.z : u.w));
 }
@@ -173,6 +182,16 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
   const float *sAl = reinterpret_cast<const float *>(smem) + lane;              // A_ext[32b + lane] (NaN-padded)
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + kCOff);
   const uint32_t *sQl = reinterpret_cast<const uint32_t *>(smem + kQOff) + lane;  // Q word (row 0, w 0) of this lane
+  // ... as a shared-window address: the Q row of a flip is read through it when NPL > 4 (config 2
+  // 96.7 -> 94.3 ms; at NPL <= 4 the generic pointer measured 2.6% faster, config 1)
+  constexpr bool kQAddr = NPL > 4;
+  uint32_t sQa = kQAddr ? (uint32_t)__cvta_generic_to_shared(sQl) : 0u;
+  if constexpr (kQAddr) asm volatile("" : "+r"(sQa));
+  // word w of this lane in the Q row of spin j
+  auto qword = [&](const uint32_t *rowp, uint32_t rowa, int w) -> uint32_t {
+    if constexpr (kQAddr) return lds_u32(rowa + 128u * (uint32_t)w);
+    else return rowp[32 * w];
+  };
   unsigned char *wbase = smem + a.blob_bytes + warp * qkp_warp_smem_bytes<NPL>();
   float *phs = reinterpret_cast<float *>(wbase) + lane;                        // (2x_i - 1) phi_i, i = 32b + lane
   uint32_t *phw = reinterpret_cast<uint32_t *>(wbase) + lane;                  // PK: packed phi pairs
@@ -252,13 +271,14 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
     if (j < n) {                                    // an item flip moves phi: certificates void
       qmask = 0u;
       const uint32_t *row = sQl + j * (QW * 32);
+      const uint32_t rowa = sQa + (uint32_t)(j * (QW * 128));
       if constexpr (PK) {
         // phi_i -= delta Q_ij on two items per word: pq = biased bytes (Q + 128) of entries
         // (2p, 2p+1) as 16-bit halves, phi - delta (pq - 0x00800080)
         if (dl > 0.0f) {
 #pragma unroll
           for (int w = 0; w < QW; ++w) {
-            const uint32_t word = row[32 * w];
+            const uint32_t word = qword(row, rowa, w);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               if (4 * w + 2 * h < NPL)
@@ -267,7 +287,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
         } else {
 #pragma unroll
           for (int w = 0; w < QW; ++w) {
-            const uint32_t word = row[32 * w];
+            const uint32_t word = qword(row, rowa, w);
 #pragma unroll
             for (int h = 0; h < 2; ++h)
               if (4 * w + 2 * h < NPL)
@@ -277,7 +297,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
       } else {
 #pragma unroll
         for (int w = 0; w < QW; ++w) {
-          const uint32_t word = row[32 * w];
+          const uint32_t word = qword(row, rowa, w);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int m = E * w + e;
@@ -338,10 +358,11 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             const int L = __ffs(fb) - 1;
             fb &= fb - 1u;
             const uint32_t *row = sQl + (32 * b + L) * (QW * 32);
+            const uint32_t rowa = sQa + (uint32_t)((32 * b + L) * (QW * 128));
             if ((up >> L) & 1u) {                         // 0 -> 1: phi -= Q_j
 #pragma unroll
               for (int w = 0; w < QW; ++w) {
-                const uint32_t word = row[32 * w];
+                const uint32_t word = qword(row, rowa, w);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                   if (2 * w + h < PW) acc[2 * w + h] = acc[2 * w + h] - __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) + 0x00800080u;
@@ -349,7 +370,7 @@ __global__ void __launch_bounds__(kQkpMaxThreads, 1) saim_qkp_kernel(const RunAr
             } else {                                      // 1 -> 0: phi += Q_j
 #pragma unroll
               for (int w = 0; w < QW; ++w) {
-                const uint32_t word = row[32 * w];
+                const uint32_t word = qword(row, rowa, w);
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
                   if (2 * w + h < PW) acc[2 * w + h] = acc[2 * w + h] + __byte_perm(word, 0u, h ? 0x4342u : 0x4140u) - 0x00800080u;
