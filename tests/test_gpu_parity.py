@@ -320,6 +320,12 @@ def test_mkp_spec_edge_cases(P, variant):
     run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=37, R=1, K=4, T=30, flags=variant)     # one replica
     q = _mkp(45, 6, 0.25, 43)
     run_both(P, [p, q], [si.paper_P(p, 5.0), si.paper_P(q, 5.0)], 0.05, 50.0, seed=38, R=13, K=3, T=25, flags=variant)
+    # a large instance (N ~ 900 spins: 14 KB of per-chain tables, few warps per CTA) with more
+    # chains than one wave of CTAs holds
+    huge = _mkp(800, 5, 0.5, 44)
+    g = run_both(P, [huge], [si.paper_P(huge, 5.0)], 0.05, 50.0, seed=39, R=700, K=2, T=6, reps=[0, 350, 699],
+                 flags=variant)
+    assert g["info"]["kernel"] == 2
 
 
 def test_mkp_spec_needs_few_constraints(P):
