@@ -75,9 +75,11 @@ inline __host__ __device__ uint32_t mkp_band_stride(int n) { return align16u((ui
 // Per-warp MKP shared memory (lockstep kernel): x bits [WN][32 lanes], logits of the current
 // 128-spin group [128][32] floats, Lambda [MM][32] int64.
 // With producer warps (prod = 1): two logit buffers [2][128][32] (groups alternate by parity) and
-// the consumer/producer mbarriers full[2], empty[2] after Lambda.
+// the consumer/producer mbarriers full[2], empty[2] after Lambda.  Last: r [MM][32] and c_l Lambda
+// [MM][32] floats, the per-lane copies the row-interleaved slack phase indexes by row.
 inline __host__ __device__ uint32_t mkp_warp_bytes(int WN, int MM, int prod = 0) {
-  return align16u((uint32_t)WN * 128u) + (prod ? 2u : 1u) * 128u * 128u + (uint32_t)MM * 256u + (prod ? 32u : 0u);
+  return align16u((uint32_t)WN * 128u) + (prod ? 2u : 1u) * 128u * 128u + (uint32_t)MM * 256u + (prod ? 32u : 0u) +
+         2u * (uint32_t)MM * 128u;
 }
 // Per-warp shared memory of the row-split kernel with S lanes per replica (G = 32/S replicas):
 // x bits [WN][G] words, logits of the current 128-spin group [128][G] floats, Lambda of each

@@ -23,6 +23,10 @@
 
 #include "saim_dev.cuh"
 
+#ifndef SAIM_MKP_SLACKB
+#define SAIM_MKP_SLACKB 4   // rows of slack bits taken interleaved
+#endif
+
 namespace saim {
 
 namespace {
@@ -123,6 +127,9 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
   // groups alternate between two buffers, loff = 0 or 4096)
   float *lt = reinterpret_cast<float *>(wbase + align16u(a.WN * 128u)) + lane;
   long long *Lam = reinterpret_cast<long long *>(wbase + align16u(a.WN * 128u) + lbytes) + lane;  // [m]
+  // per-lane copies of r and c_l Lambda indexed by row (slack phase): rs[32 m], cLs[32 m]
+  float *rs = reinterpret_cast<float *>(wbase + align16u(a.WN * 128u) + lbytes + MM * 256u + (prod ? 32u : 0u)) + lane;
+  float *cLs = rs + MM * 32;
 
   if (producer) {
     // The consumer takes the groups g = 0 .. NG-1 of every sweep t of every iteration k in order
@@ -182,6 +189,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
       cL[m] = (float)(c_l * (double)Lam[32 * m]);
+      cLs[32 * m] = cL[m];
       cLmax = fmaxf(cLmax, fabsf(cL[m]));
     }
     // |z_f32 - z| <= beta (E1 |A_i|_1 + E0_i) + 2^-23 |z|, E = (MM+8) 2^-24 (...):
@@ -335,52 +343,137 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         xw[32 * w] = xcur;
       }
       // ---- slack bits: row m, bit q, spin i = n + sum_{m'<m} q_m' + q (R4) ----
-      int i = n;
-      xcur = xw[32 * (n >> 5)];                            // word holding spin n (stored by the item loop)
-      // logit of the current slack spin, loaded one step ahead (the loads are off the decision
-      // chain; at a group boundary the new group is filled first and the logit reloaded)
-      float l = lt[loff + 32 * (n & 127)];
+      // The field of a slack bit of row m involves r_m only, and after the items r_m is moved by
+      // row m's own slack bits alone: the rows' decision sequences are independent of each other, so
+      // taking them interleaved -- SB rows at a time, bit by bit, each row's bits in order -- gives
+      // exactly the decisions of the sequential sweep (same state seen, same counter-based
+      // uniforms), with SB independent dependency chains in flight instead of one.  The rows are
+      // indexed dynamically, so r moves to per-lane shared memory for this phase (rs) and each
+      // row's slack bits are held as one register (sv).  The logits stay in the one-group buffer:
+      // a pass per 128-spin group takes the bits of every row that lie inside the group.
 #pragma unroll
-      for (int m = 0; m < MA; ++m) {
-        const int qm = (m < M) ? sQ[m] : 0;
-        for (int q = 0; q < qm; ++q, ++i) {
-          if ((i & 31) == 0) xcur = xw[32 * (i >> 5)];
-          if ((i & 127) == 0) {
-            fill_group(i >> 7);
-            l = lt[loff];
-          }
-          const float l_n = lt[loff + 32 * ((i + 1) & 127)];   // valid unless i + 1 starts a group
-          const int xb = (xcur >> (i & 31)) & 1u;
-          const float A = (float)(1u << q);
-          const float sg = xb ? -1.0f : 1.0f;
-          const float inner = fmaf(twocp, r[m], cL[m]);
-          const float F = -(A * inner) - (cpf * A) * A * sg;
-          const float z = bf * F;
-          // |z_f32 - z| <= beta (8 2^-24 + 1.01 2^-22) (A (|2 c_p r_m| + |c_l Lambda_m|) + c_p A^2)
-          const float e = bf * (8.0f * 0x1p-24f + 1.01f * 0x1p-22f) *
-                          fmaf(A, fabsf(twocp * r[m]) + fabsf(cL[m]), cpf * A * A);
-          const int nx = decide(z, e, l, [&]() -> int {
-            const uint32_t w = word_of(key, i, t, k, srho);
-            const double Ad = (double)A;
-            const double t1 = Ad * 2.0 * c_p * (double)r[m], t2 = Ad * c_l * (double)Lam[32 * m];
-            const double t3 = c_p * Ad * Ad;
-            const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
-            const int rs = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
-            if constexpr (RP) {                          // double-double level: replay kernel only
-              if ((rs & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
-                const long long Ai = 1LL << q;
-                return decide_dd(0, 2 * Ai * (long long)r[m] + Ai * Ai * (1 - 2 * xb), Ai * Lam[32 * m], a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, w);
+      for (int m = 0; m < MA; ++m) rs[32 * m] = r[m];
+      {
+        constexpr int SB = SAIM_MKP_SLACKB;
+        int mrow = 0, srow = n;                            // first unfinished row and its first spin
+        for (int g = n >> 7; 128 * g < N; ++g) {
+          if (128 * g >= n) fill_group(g);                 // (a group the items began is already filled)
+          const int glo = max(n, 128 * g), ghi = min(N, 128 * g + 128);
+          while (mrow < M && srow < ghi) {
+            float rr[SB], cl[SB];
+            uint32_t sv[SB];
+            int S[SB], qa[SB], qb[SB], qq[SB];
+            int smax = 0, sj = srow;
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+              const int m = min(mrow + j, M - 1);
+              const bool act = mrow + j < M && sj < ghi;
+              const int qm = sQ[m];
+              S[j] = sj;
+              qq[j] = qm;
+              qa[j] = act ? max(0, glo - sj) : 0;
+              qb[j] = act ? min(qm, ghi - sj) : 0;
+              rr[j] = rs[32 * m];
+              cl[j] = cLs[32 * m];
+              const int w0 = min(sj >> 5, a.WN - 1), o = sj & 31;
+              const uint32_t lo = xw[32 * w0], hi = xw[32 * min(w0 + 1, a.WN - 1)];
+              sv[j] = __funnelshift_r(lo, hi, o) & ((1u << qm) - 1u);     // (qm <= 21)
+              smax = max(smax, qb[j] - qa[j]);
+              if (mrow + j < M) sj += qm;
+            }
+            for (int st = 0; st < smax; ++st) {
+              int nxv[SB];
+              bool needv[SB];
+              bool anyneed = false;
+#pragma unroll
+              for (int j = 0; j < SB; ++j) {
+                const int q = min(qa[j] + st, 31);             // (rows past their bits: clamped, masked by on)
+                const bool on = q < qb[j];
+                const int i = S[j] + q;
+                const float l = lt[loff + 32 * (i & 127)];
+                const int xb = (sv[j] >> q) & 1u;
+                const float A = __int_as_float((127 + q) << 23);      // 2^q
+                const float sg = xb ? -1.0f : 1.0f;
+                const float inner = fmaf(twocp, rr[j], cl[j]);
+                const float F = -(A * inner) - (cpf * A) * A * sg;
+                const float z = bf * F;
+                // |z_f32 - z| <= beta (8 2^-24 + 1.01 2^-22) (A (|2 c_p r_m| + |c_l Lambda_m|) + c_p A^2)
+                const float e = bf * (8.0f * 0x1p-24f + 1.01f * 0x1p-22f) *
+                                fmaf(A, fabsf(twocp * rr[j]) + fabsf(cl[j]), cpf * A * A);
+                // the certified decision of decide(), the vote on the rare fp64 level taken once
+                // for the SB rows
+                const float satT = e + kSatThr;
+                const float certT = (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f;
+                const float d = z - l;
+                const bool sat = fabsf(z) > satT;
+                int nx = sat ? (z > 0.0f) : (d > 0.0f);
+                if (bz) nx = (int)(__float_as_uint(l) >> 31);
+                c_unif += (on && !bz && !sat) ? 1u : 0u;
+                needv[j] = on && !bz && !sat && !(fabsf(d) > certT);
+                anyneed |= needv[j];
+                nxv[j] = on ? nx : xb;
+              }
+              if (__any_sync(kFull, anyneed)) {
+#pragma unroll
+                for (int j = 0; j < SB; ++j) {
+                  if (needv[j]) {
+                    const int q = qa[j] + st, i = S[j] + q, m = mrow + j;
+                    const int xb = (sv[j] >> q) & 1u;
+                    ++c_fp64;
+                    const uint32_t w = word_of(key, i, t, k, srho);
+                    const double Ad = (double)(1u << q);
+                    const double t1 = Ad * 2.0 * c_p * (double)rr[j], t2 = Ad * c_l * (double)Lam[32 * m];
+                    const double t3 = c_p * Ad * Ad;
+                    const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
+                    int rs2 = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
+                    if constexpr (RP) {                    // double-double level: replay kernel only
+                      if ((rs2 & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
+                        const long long Ai = 1LL << q;
+                        rs2 = decide_dd(0, 2 * Ai * (long long)rr[j] + Ai * Ai * (1 - 2 * xb), Ai * Lam[32 * m],
+                                        a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, w);
+                      }
+                    }
+                    if (rs2 & 2) ++c_unc;
+                    nxv[j] = rs2 & 1;
+                  }
+                }
+              }
+#pragma unroll
+              for (int j = 0; j < SB; ++j) {
+                const int q = min(qa[j] + st, 31);
+                const uint32_t xb = (sv[j] >> q) & 1u;
+                const uint32_t fl = (uint32_t)nxv[j] ^ xb;           // (a row past its bits: nxv = xb)
+                const float A = __int_as_float((127 + q) << 23);
+                rr[j] = fmaf(fl ? (xb ? -1.0f : 1.0f) : 0.0f, A, rr[j]);
+                sv[j] ^= fl << q;
+                c_flips += fl;
               }
             }
-            return rs;
-          });
-          r[m] = fmaf((float)(nx - xb), A, r[m]);
-          xcur ^= (uint32_t)(nx != xb) << (i & 31);
-          c_flips += (nx != xb) ? 1u : 0u;
-          if ((i & 31) == 31 || i == N - 1) xw[32 * (i >> 5)] = xcur;
-          l = l_n;
+            // write back the rows of the batch that took decisions; rows completed leave the queue
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+              if (qb[j] > qa[j]) {
+                rs[32 * (mrow + j)] = rr[j];
+                const int w0 = S[j] >> 5, o = S[j] & 31;
+                const uint32_t mask = (1u << qq[j]) - 1u;
+                xw[32 * w0] = (xw[32 * w0] & ~(mask << o)) | (sv[j] << o);
+                if (o + qq[j] > 32) xw[32 * (w0 + 1)] = (xw[32 * (w0 + 1)] & ~(mask >> (32 - o))) | (sv[j] >> (32 - o));
+              }
+            }
+            // advance past the rows whose last bit lies inside this group
+            int adv = 0, snext = srow;
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+              if (mrow + j < M && S[j] + qq[j] <= ghi && adv == j) { ++adv; snext = S[j] + qq[j]; }
+            }
+            mrow += adv;
+            srow = snext;
+            if (adv < SB) break;                           // row mrow (if any) continues in the next group
+          }
         }
       }
+#pragma unroll
+      for (int m = 0; m < MA; ++m) r[m] = rs[32 * m];
     }
 
     // ---- readout of x_k: f, feasibility, trace, best, Lagrange step ----
