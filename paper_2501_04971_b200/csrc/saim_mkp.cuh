@@ -24,7 +24,10 @@
 #include "saim_dev.cuh"
 
 #ifndef SAIM_MKP_SLACKB
-#define SAIM_MKP_SLACKB 4   // rows of slack bits taken interleaved
+#define SAIM_MKP_SLACKB 4   // rows of slack bits taken interleaved at MM = 32
+#endif
+#ifndef SAIM_MKP_SLACKB_SMALL
+#define SAIM_MKP_SLACKB_SMALL 2   // ... at MM <= 16 (128-register instantiations)
 #endif
 
 namespace saim {
@@ -353,17 +356,27 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // a pass per 128-spin group takes the bits of every row that lie inside the group.
 #pragma unroll
       for (int m = 0; m < MA; ++m) rs[32 * m] = r[m];
-      {
-        constexpr int SB = SAIM_MKP_SLACKB;
+      // One batch step takes bit q of every row of the batch (a row is "on" while q is inside its
+      // bit range of this pass), so everything that depends on q alone -- A = 2^q and the
+      // products beta A, beta c_p A^2, the error-bound factors, the bit mask -- is shared by the
+      // rows and doubled from step to step (exact scalings).  z = fma(-beta A, fma(2c_p, r, c_l
+      // Lambda), -+ beta c_p A^2): 4 roundings' worth against the 12 the bound e allows (DESIGN 6.2).
+      auto slack_phase = [&](auto BZ) {
+        constexpr bool kBz = decltype(BZ)::value;          // sweep 0 (beta = 0): x = [u < 1/2], the logit's sign
+        constexpr int SB = MM >= 32 ? SAIM_MKP_SLACKB : SAIM_MKP_SLACKB_SMALL;
+        constexpr float kC = 8.0f * 0x1p-24f + 1.01f * 0x1p-22f;
+        constexpr float kLA1 = kLogitAbs * 1.0001f, kLR1 = kLogitRel * 1.0001f;
+        const float bfcp = bf * cpf, bfC = bf * kC, bfCcp = bfC * cpf;
         int mrow = 0, srow = n;                            // first unfinished row and its first spin
         for (int g = n >> 7; 128 * g < N; ++g) {
           if (128 * g >= n) fill_group(g);                 // (a group the items began is already filled)
           const int glo = max(n, 128 * g), ghi = min(N, 128 * g + 128);
+          const float *ltg = lt + loff - 32 * 128 * g;     // logit of spin i of this group: ltg[32 i]
           while (mrow < M && srow < ghi) {
             float rr[SB], cl[SB];
-            uint32_t sv[SB];
-            int S[SB], qa[SB], qb[SB], qq[SB];
-            int smax = 0, sj = srow;
+            uint32_t sv[SB], sv0[SB], onm[SB];
+            int S[SB], qq[SB];
+            int q0 = 32, q1 = 0, sj = srow;
 #pragma unroll
             for (int j = 0; j < SB; ++j) {
               const int m = min(mrow + j, M - 1);
@@ -371,88 +384,93 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
               const int qm = sQ[m];
               S[j] = sj;
               qq[j] = qm;
-              qa[j] = act ? max(0, glo - sj) : 0;
-              qb[j] = act ? min(qm, ghi - sj) : 0;
+              const int qa = act ? max(0, glo - sj) : 0;
+              const int qb = act ? min(qm, ghi - sj) : 0;
+              onm[j] = ((1u << qb) - 1u) & ~((1u << qa) - 1u);     // bits of the row taken in this pass (q < 32)
               rr[j] = rs[32 * m];
               cl[j] = cLs[32 * m];
               const int w0 = min(sj >> 5, a.WN - 1), o = sj & 31;
               const uint32_t lo = xw[32 * w0], hi = xw[32 * min(w0 + 1, a.WN - 1)];
-              sv[j] = __funnelshift_r(lo, hi, o) & ((1u << qm) - 1u);     // (qm <= 21)
-              smax = max(smax, qb[j] - qa[j]);
+              sv[j] = sv0[j] = __funnelshift_r(lo, hi, o) & ((1u << qm) - 1u);     // (qm <= 21)
+              if (qb > qa) { q0 = min(q0, qa); q1 = max(q1, qb); }
               if (mrow + j < M) sj += qm;
             }
-            for (int st = 0; st < smax; ++st) {
-              int nxv[SB];
-              bool needv[SB];
+            float A = __int_as_float((127 + min(q0, 31)) << 23);      // 2^q
+            float bA = bf * A, bcA2 = bfcp * A * A, eA = bfC * A, eA2 = bfCcp * A * A;
+            uint32_t bit = 1u << min(q0, 31);
+            for (int q = q0; q < q1; ++q) {
+              bool needv[SB], flipv[SB];
               bool anyneed = false;
 #pragma unroll
               for (int j = 0; j < SB; ++j) {
-                const int q = min(qa[j] + st, 31);             // (rows past their bits: clamped, masked by on)
-                const bool on = q < qb[j];
-                const int i = S[j] + q;
-                const float l = lt[loff + 32 * (i & 127)];
-                const int xb = (sv[j] >> q) & 1u;
-                const float A = __int_as_float((127 + q) << 23);      // 2^q
-                const float sg = xb ? -1.0f : 1.0f;
-                const float inner = fmaf(twocp, rr[j], cl[j]);
-                const float F = -(A * inner) - (cpf * A) * A * sg;
-                const float z = bf * F;
-                // |z_f32 - z| <= beta (8 2^-24 + 1.01 2^-22) (A (|2 c_p r_m| + |c_l Lambda_m|) + c_p A^2)
-                const float e = bf * (8.0f * 0x1p-24f + 1.01f * 0x1p-22f) *
-                                fmaf(A, fabsf(twocp * rr[j]) + fabsf(cl[j]), cpf * A * A);
-                // the certified decision of decide(), the vote on the rare fp64 level taken once
-                // for the SB rows
-                const float satT = e + kSatThr;
-                const float certT = (e + kLogitAbs + kLogitRel * fabsf(l)) * 1.0001f;
-                const float d = z - l;
-                const bool sat = fabsf(z) > satT;
-                int nx = sat ? (z > 0.0f) : (d > 0.0f);
-                if (bz) nx = (int)(__float_as_uint(l) >> 31);
-                c_unif += (on && !bz && !sat) ? 1u : 0u;
-                needv[j] = on && !bz && !sat && !(fabsf(d) > certT);
-                anyneed |= needv[j];
-                nxv[j] = on ? nx : xb;
+                const bool on = (onm[j] & bit) != 0u;
+                const float l = on ? ltg[32 * (S[j] + q)] : 1.0f;
+                const bool xb = (sv[j] & bit) != 0u;
+                if constexpr (kBz) {
+                  needv[j] = false;
+                  flipv[j] = on && ((__float_as_uint(l) >> 31) != 0u) != xb;
+                } else {
+                  const float s1 = fabsf(twocp * rr[j]) + fabsf(cl[j]);
+                  const float inner = fmaf(twocp, rr[j], cl[j]);
+                  const float z = fmaf(-bA, inner, xb ? bcA2 : -bcA2);
+                  // |z_f32 - z| <= beta (8 2^-24 + 1.01 2^-22) (A (|2 c_p r_m| + |c_l Lambda_m|) + c_p A^2)
+                  const float e = fmaf(eA, s1, eA2);
+                  const float satT = e + kSatThr;
+                  const float certT = fmaf(1.0001f, e, fmaf(kLR1, fabsf(l), kLA1));
+                  const float d = z - l;
+                  const bool sat = fabsf(z) > satT;
+                  const bool nx = (sat ? z : d) > 0.0f;
+                  c_unif += (on && !sat) ? 1u : 0u;
+                  needv[j] = on && !sat && !(fabsf(d) > certT);
+                  anyneed |= needv[j];
+                  flipv[j] = on && nx != xb;
+                }
               }
-              if (__any_sync(kFull, anyneed)) {
+              if constexpr (!kBz) {
+                // the rare fp64 level, one vote for the SB rows
+                if (__any_sync(kFull, anyneed)) {
 #pragma unroll
-                for (int j = 0; j < SB; ++j) {
-                  if (needv[j]) {
-                    const int q = qa[j] + st, i = S[j] + q, m = mrow + j;
-                    const int xb = (sv[j] >> q) & 1u;
-                    ++c_fp64;
-                    const uint32_t w = word_of(key, i, t, k, srho);
-                    const double Ad = (double)(1u << q);
-                    const double t1 = Ad * 2.0 * c_p * (double)rr[j], t2 = Ad * c_l * (double)Lam[32 * m];
-                    const double t3 = c_p * Ad * Ad;
-                    const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
-                    int rs2 = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
-                    if constexpr (RP) {                    // double-double level: replay kernel only
-                      if ((rs2 & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
-                        const long long Ai = 1LL << q;
-                        rs2 = decide_dd(0, 2 * Ai * (long long)rr[j] + Ai * Ai * (1 - 2 * xb), Ai * Lam[32 * m],
-                                        a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, w);
+                  for (int j = 0; j < SB; ++j) {
+                    if (needv[j]) {
+                      const int i = S[j] + q, m = mrow + j;
+                      const int xb = (sv[j] >> q) & 1u;
+                      ++c_fp64;
+                      const uint32_t w = word_of(key, i, t, k, srho);
+                      const double Ad = (double)(1u << q);
+                      const double t1 = Ad * 2.0 * c_p * (double)rr[j], t2 = Ad * c_l * (double)Lam[32 * m];
+                      const double t3 = c_p * Ad * Ad;
+                      const double zz = beta * (-t1 - t2 - t3 * (1.0 - 2.0 * xb));
+                      int rs2 = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3)), w);
+                      if constexpr (RP) {                  // double-double level: replay kernel only
+                        if ((rs2 & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
+                          const long long Ai = 1LL << q;
+                          rs2 = decide_dd(0, 2 * Ai * (long long)rr[j] + Ai * Ai * (1 - 2 * xb), Ai * Lam[32 * m],
+                                          a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, w);
+                        }
                       }
+                      if (rs2 & 2) ++c_unc;
+                      flipv[j] = (rs2 & 1) != xb;
                     }
-                    if (rs2 & 2) ++c_unc;
-                    nxv[j] = rs2 & 1;
                   }
                 }
               }
 #pragma unroll
               for (int j = 0; j < SB; ++j) {
-                const int q = min(qa[j] + st, 31);
-                const uint32_t xb = (sv[j] >> q) & 1u;
-                const uint32_t fl = (uint32_t)nxv[j] ^ xb;           // (a row past its bits: nxv = xb)
-                const float A = __int_as_float((127 + q) << 23);
-                rr[j] = fmaf(fl ? (xb ? -1.0f : 1.0f) : 0.0f, A, rr[j]);
-                sv[j] ^= fl << q;
-                c_flips += fl;
+                if (flipv[j]) {                            // r_m += delta 2^q, delta = 1 - 2 x
+                  rr[j] += (sv[j] & bit) ? -A : A;
+                  sv[j] ^= bit;
+                }
               }
+              A += A; bA += bA; eA += eA;
+              bcA2 *= 4.0f; eA2 *= 4.0f;
+              bit += bit;
             }
-            // write back the rows of the batch that took decisions; rows completed leave the queue
+            // write back the rows of the batch that took decisions (every bit is decided once per
+            // sweep, so the flips are the changed bits); rows completed leave the queue
 #pragma unroll
             for (int j = 0; j < SB; ++j) {
-              if (qb[j] > qa[j]) {
+              if (onm[j]) {
+                c_flips += __popc(sv[j] ^ sv0[j]);
                 rs[32 * (mrow + j)] = rr[j];
                 const int w0 = S[j] >> 5, o = S[j] & 31;
                 const uint32_t mask = (1u << qq[j]) - 1u;
@@ -471,7 +489,9 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
             if (adv < SB) break;                           // row mrow (if any) continues in the next group
           }
         }
-      }
+      };
+      if (bz) slack_phase(std::true_type{});
+      else slack_phase(std::false_type{});
 #pragma unroll
       for (int m = 0; m < MA; ++m) r[m] = rs[32 * m];
     }
