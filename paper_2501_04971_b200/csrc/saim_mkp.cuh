@@ -75,6 +75,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   }
 }
 
+// 16 bytes of read-only shared memory (item columns) by shared-window address
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
 template <int MM>
 struct MkpCfg {
   static constexpr int kThreads = MM <= 16 ? 512 : 256;
@@ -121,6 +128,8 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
   const int N = Hp->N;
   const MkpLayout L = mkp_layout(n, MM);
   const float *sAcol = reinterpret_cast<const float *>(smem + L.acol);
+  uint32_t acol_sa = smem_u32(sAcol);                  // the item columns as a shared-window address
+  asm volatile("" : "+r"(acol_sa));
   const float4 *sIc = reinterpret_cast<const float4 *>(smem + L.iconst);
   const int32_t *sC = reinterpret_cast<const int32_t *>(smem + L.cint);
   const long long *sB = reinterpret_cast<const long long *>(smem + L.brow);
@@ -265,14 +274,24 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // pre = A_i . r evaluated with r as it was BEFORE the decision of spin i-1 (so it is computed
       // off the sequential dependency chain, during step i-1); the exact dot follows from one fma
       // with the band value G_i = A_i . A_{i-1}:  A_i . r_now = pre + delta_{i-1} G_i.
-      auto dots = [&](int i, float &pr, float &dlv) {
-        const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
+      // A column is read from shared memory once: the lookahead of step i loads column i + 1 into
+      // registers for its dot products, and step i + 1 updates r from the same registers (two
+      // columns live, the item loop unrolled by two so they alternate without moves).  The loads go
+      // through a 32-bit shared-window address (through the generic pointer the compiler rebuilt
+      // the window base -- S2R SR_CgaCtaId, MOV, LEA -- in every step).
+      constexpr int NC4 = (MA + 3) / 4;
+      auto ldcol = [&](int i, float4 (&c)[NC4]) {
+        const uint32_t ca = acol_sa + (uint32_t)i * (MM * 4u);
+#pragma unroll
+        for (int m4 = 0; m4 < NC4; ++m4) c[m4] = lds_f4(ca + 16u * m4);
+      };
+      auto dots = [&](const float4 (&c)[NC4], float &pr, float &dlv) {
         // four partial sums per dot product (short dependency chains; each term still passes at
         // most MA/4 + 2 roundings, inside the (MM + 8) 2^-24 bound of E1)
         float dr0 = 0.f, dr1 = 0.f, dr2 = 0.f, dr3 = 0.f, dl0 = 0.f, dl1 = 0.f, dl2 = 0.f, dl3 = 0.f;
 #pragma unroll
-        for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
-          const float4 av = Ac[m4];
+        for (int m4 = 0; m4 < NC4; ++m4) {
+          const float4 av = c[m4];
           dr0 = fmaf(av.x, r[4 * m4 + 0], dr0);
           dl0 = fmaf(av.x, cL[4 * m4 + 0], dl0);
           if (4 * m4 + 1 < MA) { dr1 = fmaf(av.y, r[4 * m4 + 1], dr1); dl1 = fmaf(av.y, cL[4 * m4 + 1], dl1); }
@@ -283,65 +302,79 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         dlv = (dl0 + dl1) + (dl2 + dl3);
       };
       float pre = 0.f, dlc = 0.f, dprev = 0.f, Gc = 0.f;
-      dots(0, pre, dlc);                                  // (column n is zero: the lookahead past n-1 is harmless)
+      float4 colA[NC4], colB[NC4];
+      ldcol(0, colA);
+      dots(colA, pre, dlc);                               // (column n is zero: the lookahead past n-1 is harmless)
+      float l = 0.f, G_n = 0.f;
+      float4 ic = make_float4(0.f, 0.f, 0.f, 0.f);
+      // one item step: decision of spin i = 32 w + ii with column i in cur; the lookahead fills nxt
+      auto item_step = [&](int i, int ii, const float4 (&cur)[NC4], float4 (&nxt)[NC4]) {
+        const float l_n = lt[loff + 32 * ((i + 1) & 127)];       // valid for ii + 1 < iend (same group)
+        const float4 ic_n = sIc[i + 1];                   // padded entry n
+        const float G_nn = sBand[i + 2 <= n ? i + 2 : n];
+        const int xb = (xcur >> ii) & 1u;
+        const float dr = fmaf(dprev, Gc, pre);            // A_i . r (current state)
+        float pre_n, dl_n;
+        ldcol(i + 1, nxt);
+        dots(nxt, pre_n, dl_n);                           // lookahead (independent of this decision)
+        const float sg = xb ? -1.0f : 1.0f;               // 1 - 2 x_i
+        const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
+        const float z = bf * F;
+        const float e = bf * fmaf(E1, ic.z, ic.w);
+        const int nx = decide(z, e, l, [&]() -> int {
+          const uint32_t wd = word_of(key, i, t, k, srho);
+          double drd = 0.0, dld = 0.0, a2 = 0.0;
+#pragma unroll
+          for (int m = 0; m < MM; ++m) {
+            const double Am = (double)sAcol[i * MM + m];
+            drd += Am * (double)r[m];
+            dld += Am * (double)Lam[32 * m];
+            a2 += Am * Am;
+          }
+          const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * drd, t4 = c_l * dld;
+          const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
+          const int rs = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), wd);
+          if constexpr (RP) {                            // double-double level: replay kernel only
+            if ((rs & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
+              // double-double level on the exact integers (drd, a2 exact in fp64; kappa in int64)
+              long long kap = 0;
+              for (int m = 0; m < MA; ++m) kap += (long long)sAcol[i * MM + m] * Lam[32 * m];
+              return decide_dd(-(long long)sC[i], 2 * (long long)drd + (long long)a2 * (1 - 2 * xb), kap, a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, wd);
+            }
+          }
+          return rs;
+        });
+        const float dl = (nx != xb) ? sg : 0.0f;          // delta in {-1, 0, +1}; fma(0, A, r) == r
+#pragma unroll
+        for (int m4 = 0; m4 < NC4; ++m4) {
+          const float4 av = cur[m4];
+          r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
+          if (4 * m4 + 1 < MA) r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
+          if (4 * m4 + 2 < MA) r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
+          if (4 * m4 + 3 < MA) r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
+        }
+        xcur ^= (uint32_t)(nx != xb) << ii;
+        c_flips += (nx != xb) ? 1u : 0u;
+        pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
+        l = l_n; ic = ic_n; G_n = G_nn;
+      };
       for (int w = 0; 32 * w < n; ++w) {
         xcur = xw[32 * w];
         if ((w & 3) == 0) fill_group(w >> 2);
         const int iend = min(32, n - 32 * w);
         // state-independent operands of the current step, prefetched one step ahead
-        float l = lt[loff + 32 * ((32 * w) & 127)];
-        float4 ic = sIc[32 * w];                          // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
-        float G_n = sBand[32 * w + 1];
-        for (int ii = 0; ii < iend; ++ii) {
-          const int i = 32 * w + ii;
-          const float l_n = lt[loff + 32 * ((i + 1) & 127)];     // valid for ii + 1 < iend (same group)
-          const float4 ic_n = sIc[i + 1];                 // padded entry n
-          const float G_nn = sBand[i + 2 <= n ? i + 2 : n];
-          const int xb = (xcur >> ii) & 1u;
-          const float dr = fmaf(dprev, Gc, pre);          // A_i . r (current state)
-          float pre_n, dl_n;
-          dots(i + 1, pre_n, dl_n);                       // lookahead (independent of this decision)
-          const float sg = xb ? -1.0f : 1.0f;             // 1 - 2 x_i
-          const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
-          const float z = bf * F;
-          const float e = bf * fmaf(E1, ic.z, ic.w);
-          const int nx = decide(z, e, l, [&]() -> int {
-            const uint32_t wd = word_of(key, i, t, k, srho);
-            double drd = 0.0, dld = 0.0, a2 = 0.0;
+        l = lt[loff + 32 * ((32 * w) & 127)];
+        ic = sIc[32 * w];                                 // (-c_o c_i, c_p a_i, |A_i|_1, E0_i)
+        G_n = sBand[32 * w + 1];
+        int ii = 0;
+        for (; ii + 1 < iend; ii += 2) {
+          item_step(32 * w + ii, ii, colA, colB);
+          item_step(32 * w + ii + 1, ii + 1, colB, colA);
+        }
+        if (ii < iend) {                                  // odd tail: one step, then the next column becomes colA
+          item_step(32 * w + ii, ii, colA, colB);
 #pragma unroll
-            for (int m = 0; m < MM; ++m) {
-              const double Am = (double)sAcol[i * MM + m];
-              drd += Am * (double)r[m];
-              dld += Am * (double)Lam[32 * m];
-              a2 += Am * Am;
-            }
-            const double t1 = c_o * (double)sC[i], t2 = c_p * a2, t3 = 2.0 * c_p * drd, t4 = c_l * dld;
-            const double zz = beta * (-t1 - t2 * (1.0 - 2.0 * xb) - t3 - t4);
-            const int rs = certify_fp64(zz, beta * (fabs(t1) + fabs(t2) + fabs(t3) + fabs(t4)), wd);
-            if constexpr (RP) {                          // double-double level: replay kernel only
-              if ((rs & 2) || (a.flags & SAIM_FLAG_TEST_REPLAY)) {
-                // double-double level on the exact integers (drd, a2 exact in fp64; kappa in int64)
-                long long kap = 0;
-                for (int m = 0; m < MA; ++m) kap += (long long)sAcol[i * MM + m] * Lam[32 * m];
-                return decide_dd(-(long long)sC[i], 2 * (long long)drd + (long long)a2 * (1 - 2 * xb), kap, a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, wd);
-              }
-            }
-            return rs;
-          });
-          const float dl = (float)(nx - xb);              // delta in {-1, 0, +1}; fma(0, A, r) == r
-          const float4 *Ac = reinterpret_cast<const float4 *>(sAcol + i * MM);
-#pragma unroll
-          for (int m4 = 0; m4 < (MA + 3) / 4; ++m4) {
-            const float4 av = Ac[m4];
-            r[4 * m4 + 0] = fmaf(dl, av.x, r[4 * m4 + 0]);
-            if (4 * m4 + 1 < MA) r[4 * m4 + 1] = fmaf(dl, av.y, r[4 * m4 + 1]);
-            if (4 * m4 + 2 < MA) r[4 * m4 + 2] = fmaf(dl, av.z, r[4 * m4 + 2]);
-            if (4 * m4 + 3 < MA) r[4 * m4 + 3] = fmaf(dl, av.w, r[4 * m4 + 3]);
-          }
-          xcur ^= (uint32_t)(nx != xb) << ii;
-          c_flips += (nx != xb) ? 1u : 0u;
-          pre = pre_n; dlc = dl_n; Gc = G_n; dprev = dl;
-          l = l_n; ic = ic_n; G_n = G_nn;
+          for (int m4 = 0; m4 < NC4; ++m4) colA[m4] = colB[m4];
         }
         xw[32 * w] = xcur;
       }
