@@ -26,6 +26,9 @@
 #ifndef SAIM_MKP_SLACKB
 #define SAIM_MKP_SLACKB 4   // rows of slack bits taken interleaved at MM = 32
 #endif
+#ifndef SAIM_MKP_FILL_UNROLL
+#define SAIM_MKP_FILL_UNROLL 4   // Philox calls in flight per lane when a group's logits are drawn
+#endif
 #ifndef SAIM_MKP_SLACKB_SMALL
 #define SAIM_MKP_SLACKB_SMALL 2   // ... at MM <= 16 (128-register instantiations)
 #endif
@@ -35,6 +38,7 @@ namespace saim {
 namespace {
 
 constexpr uint32_t kFull = 0xffffffffu;
+constexpr int kFillUnroll = SAIM_MKP_FILL_UNROLL;
 
 // fp64 tail of the slow path: z and its magnitude sum S are accurate to ~2^-50 S; returns
 // (x | uncertified << 1).
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // not depend on the state, so they are drawn in one ILP-friendly burst per group, off the
       // sequential dependency chain of the decisions.
       auto fill_words = [&](int g, auto NW) {              // NW = words of the group holding spins
-#pragma unroll 4
+#pragma unroll kFillUnroll
         for (int j = 0; j < 32; ++j) {
           const uint4 w4 = philox_group(key, g, j, t, k, srho);
           lt[32 * (j + 0)] = logit_signed(w4.x);

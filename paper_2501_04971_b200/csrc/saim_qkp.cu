@@ -109,7 +109,8 @@ __global__ void selftest_logit_kernel(unsigned long long *out) {
   const double u = uniform_f64(w);
   const double l = log(u) - log1p(-u);
   const double err = fabs((double)lf - l);
-  const double rel = err / ((double)kLogitAbs + (double)kLogitRel * fabs(l));
+  double rel = err / ((double)kLogitAbs + (double)kLogitRel * fabs(l));
+  if ((double)uniform_f32(w) != u) rel = 1e30;     // the fp32 uniform must be the exact (2m + 1) 2^-24
   atomicMax(out + 0, (unsigned long long)__double_as_longlong(rel));   // non-negative doubles order as ints
   atomicMax(out + 1, (unsigned long long)__double_as_longlong(err));
 }
