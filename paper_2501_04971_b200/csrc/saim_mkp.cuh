@@ -224,15 +224,31 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
       // (32g + j, t, k, s<<20|rho) yields the words of spins 128g + 32w + j, w = 0..3).  They do
       // not depend on the state, so they are drawn in one ILP-friendly burst per group, off the
       // sequential dependency chain of the decisions.
+      // Software-pipelined by one step of 4 calls: the logits (two MUFU each, XU pipe) of the
+      // previous 4 calls are taken next to the Philox rounds (IMAD/LOP3) of the next 4, so a warp
+      // alone on its SMSP has both pipes busy instead of one after the other.
       auto fill_words = [&](int g, auto NW) {              // NW = words of the group holding spins
-#pragma unroll kFillUnroll
-        for (int j = 0; j < 32; ++j) {
-          const uint4 w4 = philox_group(key, g, j, t, k, srho);
+        auto put = [&](int j, const uint4 &w4) {
           lt[32 * (j + 0)] = logit_signed(w4.x);
           if (NW.value > 1) lt[32 * (j + 32)] = logit_signed(w4.y);
           if (NW.value > 2) lt[32 * (j + 64)] = logit_signed(w4.z);
           if (NW.value > 3) lt[32 * (j + 96)] = logit_signed(w4.w);
+        };
+        uint4 wq[kFillUnroll];
+#pragma unroll
+        for (int b = 0; b < kFillUnroll; ++b) wq[b] = philox_group(key, g, b, t, k, srho);
+#pragma unroll 1
+        for (int j0 = kFillUnroll; j0 < 32; j0 += kFillUnroll) {
+          uint4 wn[kFillUnroll];
+#pragma unroll
+          for (int b = 0; b < kFillUnroll; ++b) wn[b] = philox_group(key, g, j0 + b, t, k, srho);
+#pragma unroll
+          for (int b = 0; b < kFillUnroll; ++b) put(j0 - kFillUnroll + b, wq[b]);
+#pragma unroll
+          for (int b = 0; b < kFillUnroll; ++b) wq[b] = wn[b];
         }
+#pragma unroll
+        for (int b = 0; b < kFillUnroll; ++b) put(32 - kFillUnroll + b, wq[b]);
       };
       auto fill_group = [&](int g) {
         if (prod) {                                        // the producer's buffer (g & 1)
