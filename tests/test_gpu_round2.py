@@ -10,6 +10,7 @@
 * API hygiene: the per-launch shared-memory attribute (a later, smaller saim_create of the same
   kernel template must not break an earlier context) and output-buffer validation.
 """
+import dataclasses
 import math
 from concurrent.futures import ThreadPoolExecutor
 from fractions import Fraction
@@ -275,3 +276,30 @@ def test_logit_table_matches_direct_computation(P):
     host = np.log(u) - np.log1p(-u)
     assert np.all(np.abs(tab - host) <= 4 * np.spacing(np.abs(host)) + 1e-300)
     assert tab[4] < 0 < tab[5]                           # u < 1/2 <=> w < 2^31
+
+
+# ---------------------------------------------------------------------------------------------
+# Row-interleaved slack phase of the MKP lockstep kernel: rows of very different
+# slack widths, slack ranges that start exactly at / straddle a 128-spin group boundary, a spin
+# count that is a multiple of 32, more rows than one batch and one group hold.
+
+def _mkp_caps(n, m, caps, seed):
+    """MKP instance with hand-set capacities (slack widths = bit lengths of caps)."""
+    p = _mkp(n, m, 0.5, seed)
+    b = np.array([caps[i % len(caps)] for i in range(m)], dtype=np.int64)
+    return dataclasses.replace(p, b=b, name=f"mkp_caps_n{n}_m{m}")
+
+
+@pytest.mark.parametrize("variant", [2, 2 | 64], ids=["lockstep", "lockstep_noprod"])
+@pytest.mark.parametrize("n,m,caps", [
+    (128, 30, [1, 3, 100000, 7, 65535, 2, 40000]),        # slack starts at a group boundary; widths 1..17
+    (120, 30, [255, 255, 255, 255]),                      # 8-bit rows: 15 rows per group, several batches
+    (96, 16, [1 << 20, 1, (1 << 20) - 1, 5]),             # 21-bit rows straddling the group boundary
+    (100, 5, [4095, 1, 70000, 3, 2047]),                  # M <= 8 instantiation (2 rows per batch)
+    (101, 12, [(1 << 17) - 1] * 12),                      # MM = 16, N = 101 + 12 * 17 = 305
+    (107, 9, [(1 << 17) - 1] * 8 + [(1 << 13) - 1]),      # N = 107 + 8 * 17 + 13 = 256: a multiple of 32 and 128
+])
+def test_mkp_lockstep_slack_rows_edge_cases(P, n, m, caps, variant):
+    p = _mkp_caps(n, m, caps, 31)
+    g = run_both(P, [p], [si.paper_P(p, 5.0)], 0.05, 50.0, seed=9, R=40, K=5, T=40, flags=variant)
+    assert g["info"]["kernel"] == 2 and g["info"]["lanes_per_replica"] == 1
