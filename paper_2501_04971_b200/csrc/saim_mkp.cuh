@@ -279,10 +279,12 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         if (bz) nx = (int)(__float_as_uint(l) >> 31);     // beta_0 = 0: u < 1/2 (sign bit, -0 included)
         c_unif += (!bz && !sat) ? 1u : 0u;
         const bool need = !bz && !sat && !(fabsf(d) > certT);
+        // (the whole warp takes the slow path when some lane needs it -- its result is used by those
+        // lanes only: a warp-uniform branch, so the common path carries no reconvergence barrier)
         if (__any_sync(kFull, need)) {
+          const int rs = slow();
           if (need) {
             ++c_fp64;
-            const int rs = slow();
             if (rs & 2) ++c_unc;
             nx = rs & 1;
           }
@@ -484,10 +486,9 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
                 if (__any_sync(kFull, anyneed)) {
 #pragma unroll
                   for (int j = 0; j < SB; ++j) {
-                    if (needv[j]) {
-                      const int i = S[j] + q, m = mrow + j;
+                    if (__any_sync(kFull, needv[j])) {       // (warp-uniform, as in decide())
+                      const int i = S[j] + q, m = min(mrow + j, M - 1);
                       const int xb = (sv[j] >> q) & 1u;
-                      ++c_fp64;
                       const uint32_t w = word_of(key, i, t, k, srho);
                       const double Ad = (double)(1u << q);
                       const double t1 = Ad * 2.0 * c_p * (double)rr[j], t2 = Ad * c_l * (double)Lam[32 * m];
@@ -501,8 +502,11 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
                                           a.T >= 2 ? t : 1, a.T >= 2 ? a.T - 1 : 1, Hp, w);
                         }
                       }
-                      if (rs2 & 2) ++c_unc;
-                      flipv[j] = (rs2 & 1) != xb;
+                      if (needv[j]) {
+                        ++c_fp64;
+                        if (rs2 & 2) ++c_unc;
+                        flipv[j] = (rs2 & 1) != xb;
+                      }
                     }
                   }
                 }
