@@ -339,6 +339,11 @@ __global__ void __launch_bounds__(MkpCfg<MM>::kThreads, 1) saim_mkp_kernel(const
         float pre_n, dl_n;
         ldcol(i + 1, nxt);
         dots(nxt, pre_n, dl_n);                           // lookahead (independent of this decision)
+#ifndef SAIM_MKP_NO_PIN
+        // keep the lookahead's FMAs ahead of the slow-path branch, next to the decision chain they
+        // are meant to overlap (in one of the two unrolled steps the compiler sank them behind it)
+        asm volatile("" : "+f"(pre_n), "+f"(dl_n));
+#endif
         const float sg = xb ? -1.0f : 1.0f;               // 1 - 2 x_i
         const float F = fmaf(-twocp, dr, fmaf(-ic.y, sg, ic.x)) - dlc;
         const float z = bf * F;
