@@ -7,6 +7,10 @@
 // flip rate of MKP anneals costs nothing extra -- while the instance data a step needs (the item
 // column A_{.i}, its constants) is the same for all lanes: one shared-memory broadcast.
 //
+// Items are decided one after the other; the slack bits of different rows, whose fields involve
+// their own row's residual only, are decided interleaved (the rows' sequences are independent once
+// the items are done, so the decisions are those of the sequential sweep).
+//
 // Field of spin i (R1), with r = A_ext x - b, Lambda the Lagrange accumulator (R10):
 //   item i:   F_i = -c_o c_i - c_p a_i (1 - 2x_i) - 2 c_p (A_{.i} . r) - c_l (A_{.i} . Lambda)
 //   slack bit q of row m (A = 2^q):  F = -A (2 c_p r_m + c_l Lambda_m) - c_p A^2 (1 - 2x)
